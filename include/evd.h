@@ -1,0 +1,130 @@
+/*
+ * evd.h -- C ABI of the B200 bound-evaluation library (libevd.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `eventdiv`
+ * (arXiv 2209.13168, /root/reference/pkg).  The reference exposes this path
+ * only as Python functions; each entry point below names the reference
+ * function it replaces (file:line under pkg/src/eventdiv/).  The Python mirror
+ * of that interface is paper_2209_13168_b200/ (contrast.py, solver.py, ...),
+ * bound through ctypes in paper_2209_13168_b200/_lib.py; INTEGRATION.md shows
+ * how the reference package would bind the same symbols.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; host buffers are caller-owned and never retained.
+ *  - Every call is synchronous w.r.t. its outputs (it returns after the
+ *    results are in the caller's buffers) and runs on the context's stream.
+ *  - Return value: EVD_OK or an EVD_ERR_* code; evd_last_error() has the text.
+ *    No C++ exception crosses the ABI.
+ *  - One context per (device, host thread).  Contexts are independent.
+ *  - Arithmetic is IEEE binary64, round-to-nearest, no FMA contraction:
+ *    integer images and bounds are bit-identical to the reference's.
+ */
+#ifndef EVD_H
+#define EVD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct evd_ctx evd_ctx;
+
+enum {
+    EVD_OK = 0,
+    EVD_ERR_CUDA = 1,         /* CUDA runtime failure (message has the CUDA error) */
+    EVD_ERR_ARG = 2,          /* ValueError in the reference (bad tau/epsilon/sizes) */
+    EVD_ERR_NO_EVENTS = 3,    /* NoEventsError, solver.py:32-33,88-89 */
+    EVD_ERR_CHEIRALITY = 4,   /* CheiralityError, geometry.py:21-22,72-74 (1 + nu*tau <= 0) */
+    EVD_ERR_ITER_LIMIT = 5,   /* IterationLimitError, solver.py:36-46,118-119; result holds the incumbent */
+    EVD_ERR_STATE = 6         /* call order (e.g. no events set) */
+};
+
+/* ---- context ----------------------------------------------------------- */
+int evd_create(int device, evd_ctx **out);
+void evd_destroy(evd_ctx *ctx);
+/* Last error text for ctx (or for the calling thread when ctx is NULL). */
+const char *evd_last_error(const evd_ctx *ctx);
+/* Run subsequent work on a caller-owned cudaStream_t (NULL = the ctx's own stream). */
+int evd_set_stream(evd_ctx *ctx, void *cuda_stream);
+/* Number of kernels this context has launched so far. */
+int64_t evd_kernel_launches(const evd_ctx *ctx);
+/* SM count of the context's device. */
+int evd_device_sms(const evd_ctx *ctx);
+
+/* ---- event window (EventBatch, events.py:93-120) ---------------------- */
+/* Copies one window's SoA events (x, y, t in [0, tau]) to device memory; they
+ * stay resident for every following evaluation until the next call. */
+int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                   int32_t width, int32_t height, double tau);
+
+/* ---- motion model ------------------------------------------------------ */
+/* radial_warp (geometry.py:78-87) of n arbitrary points. */
+int evd_radial_warp(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                    double nu, double tau, int32_t width, int32_t height, double *x_out,
+                    double *y_out);
+
+/* warp_scale (geometry.py:70-75): s = (1 + nu*t) / (1 + nu*tau) for n times. */
+int evd_warp_scale(evd_ctx *ctx, const double *t, int64_t n, double nu, double tau,
+                   double *s_out);
+
+/* ---- objective and bounds on the resident window ----------------------- */
+/* accumulate_image (contrast.py:48-58) + image_contrast (contrast.py:61-64) /
+ * contrast_at (solver.py:74-76) at k velocities.  counts (nullable) receives
+ * k row-major (height, width) uint32 images. */
+int evd_point_images(evd_ctx *ctx, const double *nu, int32_t k, int64_t *in_image,
+                     double *contrast, uint32_t *counts);
+
+/* upper_bound_image (contrast.py:231-238) / bound_terms (contrast.py:241-251)
+ * for k intervals [lo_j, hi_j]: s_bar = sum(H_bar^2) (exact), fully_inside
+ * (contrast.py:195-201), marks = sum(H_bar) (= upper_bound_image().in_image_events).
+ * counts (nullable) receives k uint32 images.  c_bar is assembled by the
+ * caller as s_bar/M - (fully_inside/M)**2 exactly as contrast.py:248-251. */
+int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
+                     uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks,
+                     uint32_t *counts);
+
+/* image_contrast (contrast.py:61-64) of a caller image: np.sum((c - mean)**2)/M
+ * with numpy's pairwise summation order; mean = in_image / m. */
+int evd_image_contrast(evd_ctx *ctx, const double *counts, int64_t m, int64_t in_image,
+                       double *contrast);
+
+/* rasterize_segment (contrast.py:206-222) for k segments (ax, ay, bx, by);
+ * counts receives k uint32 (height, width) mark images (each mark 0/1). */
+int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t width,
+                           int32_t height, uint32_t *counts);
+
+/* ---- branch and bound (maximise_contrast_bnb, solver.py:79-123) -------- */
+typedef struct {
+    double gamma;               /* SolverParams.gamma (solver.py:51) */
+    double epsilon;             /* SolverParams.epsilon */
+    double min_interval_width;  /* SolverParams.min_interval_width */
+    int64_t max_iterations;     /* SolverParams.max_iterations */
+} evd_solve_params;
+
+typedef struct {
+    double nu;            /* BnbResult.nu */
+    double contrast;      /* BnbResult.contrast */
+    double bound_gap;     /* BnbResult.bound_gap */
+    int64_t iterations;   /* BnbResult.iterations */
+    int64_t bound_evals;  /* bound_terms evaluations (root + 2 per expanded node) */
+    int64_t point_evals;  /* contrast_at evaluations */
+    int64_t max_frontier; /* largest live queue */
+    double device_ms;     /* device time of the solve (CUDA events on the ctx stream) */
+} evd_solve_result;
+
+/* Whole solve on the device for the resident window (one cooperative
+ * persistent launch).  Returns EVD_ERR_ITER_LIMIT with the incumbent in *res
+ * when max_iterations is reached. */
+int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res);
+
+/* ---- helpers ----------------------------------------------------------- */
+/* out[f] = pow(f / m, 2.0) through the process's libm pow(), f = 0..n: the
+ * value CPython's `mu_lower**2` yields (contrast.py:250-251). */
+int evd_pow2_table(int64_t m, int64_t n, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EVD_H */

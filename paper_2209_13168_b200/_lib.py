@@ -1,0 +1,165 @@
+"""ctypes binding of libevd.so (the C ABI in include/evd.h).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+usable, every entry point raises ``EvdUnavailable``.  One device context is
+kept per (host thread, device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libevd.so")
+
+EVD_OK, EVD_ERR_CUDA, EVD_ERR_ARG, EVD_ERR_NO_EVENTS = 0, 1, 2, 3
+EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
+
+# every symbol include/evd.h declares (checked by tests/test_abi.py)
+SYMBOLS = (
+    "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
+    "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
+    "evd_point_images", "evd_bound_images", "evd_image_contrast", "evd_rasterize_segments",
+    "evd_solve", "evd_pow2_table",
+)
+
+
+class EvdUnavailable(RuntimeError):
+    """libevd.so could not be loaded or no CUDA device is usable."""
+
+
+class EvdError(RuntimeError):
+    """A CUDA-side failure reported by libevd."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class SolveParams(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("epsilon", ctypes.c_double),
+                ("min_interval_width", ctypes.c_double), ("max_iterations", ctypes.c_int64)]
+
+
+class SolveResult(ctypes.Structure):
+    _fields_ = [("nu", ctypes.c_double), ("contrast", ctypes.c_double),
+                ("bound_gap", ctypes.c_double), ("iterations", ctypes.c_int64),
+                ("bound_evals", ctypes.c_int64), ("point_evals", ctypes.c_int64),
+                ("max_frontier", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+
+
+_d = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_f64 = ctypes.c_double
+
+_SIGS = {
+    "evd_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "evd_destroy": (None, [_vp]),
+    "evd_last_error": (ctypes.c_char_p, [_vp]),
+    "evd_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "evd_kernel_launches": (_i64, [_vp]),
+    "evd_device_sms": (ctypes.c_int, [_vp]),
+    "evd_set_events": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64]),
+    "evd_radial_warp": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _f64, _f64, _i32, _i32, _d, _d]),
+    "evd_warp_scale": (ctypes.c_int, [_vp, _d, _i64, _f64, _f64, _d]),
+    "evd_point_images": (ctypes.c_int, [_vp, _d, _i32, _i64p, _d, _u32p]),
+    "evd_bound_images": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p, _u32p]),
+    "evd_image_contrast": (ctypes.c_int, [_vp, _d, _i64, _i64, _d]),
+    "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _u32p]),
+    "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
+    "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+_tls = threading.local()
+_default_device = int(os.environ.get("EVD_DEVICE", "0"))
+
+
+def load():
+    """Load libevd.so and declare its signatures (no device is touched)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise EvdUnavailable(
+                    f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; "
+                    f"g.build()'` (make -C paper_2209_13168_b200/csrc)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def set_device(device: int) -> None:
+    """Device used by contexts created afterwards in this process."""
+    global _default_device
+    _default_device = int(device)
+
+
+class Context:
+    """One libevd context (device buffers, stream) for the calling thread."""
+
+    def __init__(self, device: int):
+        self.lib = load()
+        h = _vp()
+        rc = self.lib.evd_create(device, ctypes.byref(h))
+        if rc != EVD_OK:
+            msg = self.lib.evd_last_error(None).decode()
+            raise EvdUnavailable(f"evd_create(device={device}) failed: {msg}")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.evd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def error_text(self) -> str:
+        return self.lib.evd_last_error(self.h).decode()
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.evd_kernel_launches(self.h))
+
+    @property
+    def sms(self) -> int:
+        return int(self.lib.evd_device_sms(self.h))
+
+
+def context(device: int | None = None) -> Context:
+    """The calling thread's context for `device` (default: set_device / EVD_DEVICE / 0)."""
+    dev = _default_device if device is None else int(device)
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    ctx = cache.get(dev)
+    if ctx is None:
+        ctx = cache[dev] = Context(dev)
+    return ctx
+
+
+def ptr(a: np.ndarray, kind=_d):
+    return a.ctypes.data_as(kind)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)

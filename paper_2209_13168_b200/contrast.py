@@ -1,0 +1,184 @@
+"""Motion-compensated event images, the contrast objective and its interval bound.
+
+Drop-in for ``pkg/src/eventdiv/contrast.py``.  Every image is built on the
+B200 (libevd.so, include/evd.h); the host only assembles the scalar bound
+``c_bar = s_bar/M - mu_lower**2`` exactly as ``contrast.py:248-251`` does, from
+the exact integers the device returns.
+
+Beyond the reference API this module adds batched forms used by the batched
+frontier and the grid oracle: ``point_terms`` (k velocities) and
+``bound_terms_many`` (k intervals) over one resident window.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .events import EventBatch, SensorGeometry
+from .geometry import CheiralityError, VelocityInterval
+
+
+@dataclass(frozen=True)
+class EventImage:
+    """Per-pixel counts (height x width) and in-image event count (contrast.py:23-36)."""
+
+    counts: np.ndarray
+    in_image_events: int
+
+    @property
+    def n_pixels(self) -> int:
+        return self.counts.size
+
+    @property
+    def mean(self) -> float:
+        return self.in_image_events / self.counts.size
+
+
+@dataclass(frozen=True)
+class ContrastBound:
+    """c_bar = s_bar/M - mu_lower^2 (contrast.py:39-45)."""
+
+    s_bar: float
+    mu_lower: float
+    c_bar: float
+
+
+def _raise(ctx, rc):
+    if rc == _lib.EVD_ERR_CHEIRALITY:
+        raise CheiralityError(ctx.error_text())
+    if rc == _lib.EVD_ERR_ARG:
+        raise ValueError(ctx.error_text())
+    raise _lib.EvdError(rc, ctx.error_text())
+
+
+def load_window(batch: EventBatch, ctx=None):
+    """Copy a window's events to the device (evd_set_events); returns the context."""
+    ctx = ctx or _lib.context()
+    g = batch.geometry
+    x, y, t = _lib.f64(batch.x), _lib.f64(batch.y), _lib.f64(batch.t)
+    rc = ctx.lib.evd_set_events(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t), t.size,
+                                g.width, g.height, float(batch.tau))
+    if rc:
+        _raise(ctx, rc)
+    return ctx
+
+
+def point_terms(batch: EventBatch, nus, images: bool = False, ctx=None, loaded=False,
+                with_contrast: bool = True):
+    """accumulate_image + image_contrast at every nu in ``nus`` on the device.
+
+    Returns (in_image int64[k], contrast float64[k], counts uint32[k, H, W] | None).
+    """
+    g = batch.geometry
+    nu = _lib.f64(np.atleast_1d(nus))
+    ctx = ctx if loaded else load_window(batch, ctx)
+    k = nu.size
+    inside = np.empty(k, dtype=np.int64)
+    con = np.empty(k, dtype=np.float64)
+    counts = np.empty((k, g.height, g.width), dtype=np.uint32) if images else None
+    rc = ctx.lib.evd_point_images(ctx.h, _lib.ptr(nu), k, _lib.ptr(inside, _lib._i64p),
+                                  _lib.ptr(con) if with_contrast else None,
+                                  _lib.ptr(counts, _lib._u32p) if images else None)
+    if rc:
+        _raise(ctx, rc)
+    return inside, con, counts
+
+
+def bound_terms_many(batch: EventBatch, lo, hi, images: bool = False, ctx=None, loaded=False):
+    """Exact bound integers for k intervals [lo_j, hi_j] on the device.
+
+    Returns (s_bar uint64[k], fully_inside int64[k], marks uint64[k],
+    counts uint32[k, H, W] | None).
+    """
+    g = batch.geometry
+    lo, hi = _lib.f64(np.atleast_1d(lo)), _lib.f64(np.atleast_1d(hi))
+    ctx = ctx if loaded else load_window(batch, ctx)
+    k = lo.size
+    s_bar = np.empty(k, dtype=np.uint64)
+    fi = np.empty(k, dtype=np.int64)
+    marks = np.empty(k, dtype=np.uint64)
+    counts = np.empty((k, g.height, g.width), dtype=np.uint32) if images else None
+    rc = ctx.lib.evd_bound_images(ctx.h, _lib.ptr(lo), _lib.ptr(hi), k,
+                                  _lib.ptr(s_bar, _lib._u64p), _lib.ptr(fi, _lib._i64p),
+                                  _lib.ptr(marks, _lib._u64p),
+                                  _lib.ptr(counts, _lib._u32p) if images else None)
+    if rc:
+        _raise(ctx, rc)
+    return s_bar, fi, marks, counts
+
+
+def assemble_bound(s_bar_int: int, fully_inside: int, m: int) -> ContrastBound:
+    """contrast.py:248-251 on the exact device integers (host CPython floats)."""
+    s_bar = float(s_bar_int)
+    mu_lower = fully_inside / m
+    return ContrastBound(s_bar, mu_lower, s_bar / m - mu_lower**2)
+
+
+def accumulate_image(batch: EventBatch, nu: float) -> EventImage:
+    """Warp every event to the batch end and bin by floor (contrast.py:48-58)."""
+    inside, _, counts = point_terms(batch, [float(nu)], images=True, with_contrast=False)
+    return EventImage(counts[0].astype(np.float64), int(inside[0]))
+
+
+def _device_contrast(counts: np.ndarray, in_image: int) -> float:
+    c = _lib.f64(counts.ravel())
+    out = np.empty(1, dtype=np.float64)
+    ctx = _lib.context()
+    rc = ctx.lib.evd_image_contrast(ctx.h, _lib.ptr(c), c.size, int(in_image), _lib.ptr(out))
+    if rc:
+        _raise(ctx, rc)
+    return float(out[0])
+
+
+def image_contrast(image: EventImage) -> float:
+    """Variance of the counts about the in-image mean (contrast.py:61-64), with
+    numpy's pairwise summation order reproduced on the device."""
+    return _device_contrast(np.asarray(image.counts), image.in_image_events)
+
+
+def image_contrast_expanded(image: EventImage) -> float:
+    """(1/M) * sum(H^2) - mean^2 (contrast.py:67-70)."""
+    mu = image.mean
+    return float(_device_contrast(np.asarray(image.counts), 0) - mu * mu)
+
+
+def rasterize_segment(p0: tuple[float, float], p1: tuple[float, float],
+                      geometry: SensorGeometry) -> set[tuple[int, int]]:
+    """Pixels whose closed squares meet the closed segment p0->p1 (contrast.py:206-222)."""
+    return rasterize_segments([(p0[0], p0[1], p1[0], p1[1])], geometry)[0]
+
+
+def rasterize_segments(segments, geometry: SensorGeometry) -> list[set[tuple[int, int]]]:
+    """Batched rasterize_segment: one device launch for all segments."""
+    segs = _lib.f64(np.asarray(segments, dtype=np.float64).reshape(-1, 4))
+    k = segs.shape[0]
+    if k == 0:
+        return []
+    counts = np.empty((k, geometry.height, geometry.width), dtype=np.uint32)
+    ctx = _lib.context()
+    rc = ctx.lib.evd_rasterize_segments(ctx.h, _lib.ptr(segs), k, geometry.width,
+                                        geometry.height, _lib.ptr(counts, _lib._u32p))
+    if rc:
+        _raise(ctx, rc)
+    if counts.max(initial=0) > 1:
+        raise _lib.EvdError(_lib.EVD_ERR_CUDA, "supercover marked a pixel twice for one segment")
+    out = []
+    for j in range(k):
+        ys, xs = np.nonzero(counts[j])
+        out.append({(int(a), int(b)) for a, b in zip(xs, ys)})
+    return out
+
+
+def upper_bound_image(batch: EventBatch, interval: VelocityInterval) -> EventImage:
+    """Per-pixel count of events whose endpoint segment touches the pixel (contrast.py:231-238)."""
+    _, _, marks, counts = bound_terms_many(batch, [interval.lo], [interval.hi], images=True)
+    return EventImage(counts[0].astype(np.float64), int(marks[0]))
+
+
+def bound_terms(batch: EventBatch, interval: VelocityInterval) -> ContrastBound:
+    """Contrast upper bound over the interval (contrast.py:241-251)."""
+    s_bar, fi, _, _ = bound_terms_many(batch, [interval.lo], [interval.hi])
+    return assemble_bound(int(s_bar[0]), int(fi[0]), batch.geometry.n_pixels)

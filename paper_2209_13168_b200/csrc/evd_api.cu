@@ -1,0 +1,727 @@
+// evd_api.cu -- host side of the C ABI declared in include/evd.h.
+//
+// Owns device buffers per context, the fixed numpy pairwise-summation plan per
+// image size, the libm pow table for the bound assembly, and the launch of the
+// device-resident branch and bound.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/evd.h"
+#include "evd_device.cuh"
+#include "evd_internal.h"
+
+using namespace evd;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t ensure(size_t n)
+    {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(n, 1);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Host plan of numpy's pairwise tree for M summands, uploaded as TreeDev.
+struct TreePlan {
+    long long M = -1;
+    int cuts_target = -1;
+    DevBuf<int2> leaves;
+    DevBuf<int> cut_leaf0, cut_trip0, cut_lvl, cut_nlev, top_lvl;
+    DevBuf<int4> trip, top;
+    DevBuf<double> cutval;
+    TreeDev dev{};
+};
+
+}  // namespace
+
+struct evd_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    long long launches = 0;
+    // resident window
+    long long n = -1;
+    int W = 0, H = 0;
+    double tau = 0.0;
+    DevBuf<double> xc, yc, t;
+    // scratch
+    DevBuf<unsigned int> img;          // 3 images (P, A, B)
+    DevBuf<unsigned long long> acc;    // 8 accumulators
+    DevBuf<double> dscratch;           // misc device doubles
+    DevBuf<double> wx, wy, wt, wxo, wyo;
+    DevBuf<double> segs;
+    DevBuf<unsigned int> seg_counts;
+    TreePlan tree;
+    // bound assembly table pow(f/M, 2)
+    DevBuf<double> pow2;
+    long long pow_m = -1, pow_n = -1;
+    // solve
+    DevBuf<SolveState> state;
+    DevBuf<FrontierEntry> frontier;
+    DevBuf<GridBar> bar;
+    int solve_blocks = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+int fail(evd_ctx *ctx, int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    g_thread_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(ctx, EVD_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+#define LAUNCHED(k)                                                                          \
+    do {                                                                                     \
+        ctx->launches += (k);                                                                \
+        cudaError_t e_ = cudaGetLastError();                                                 \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(ctx, EVD_ERR_CUDA, "kernel launch: %s (%s:%d)",                      \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+// ---- numpy pairwise tree plan (loops_utils.h.src pairwise_sum)
+struct PNode {
+    long long off, n;
+    int l, r, h;
+};
+
+int pbuild(std::vector<PNode> &v, long long off, long long n)
+{
+    const int id = (int)v.size();
+    v.push_back({off, n, -1, -1, 0});
+    if (n > 128) {  // numpy: n2 = n / 2; n2 -= n2 % 8; pw(a, n2) + pw(a + n2, n - n2)
+        long long n2 = n / 2;
+        n2 -= n2 % 8;
+        const int l = pbuild(v, off, n2);
+        const int r = pbuild(v, off + n2, n - n2);
+        v[id].l = l;
+        v[id].r = r;
+        v[id].h = 1 + std::max(v[l].h, v[r].h);
+    }
+    return id;
+}
+
+void pcuts(const std::vector<PNode> &v, int id, long long T, std::vector<int> &cuts)
+{
+    if (v[id].l < 0 || v[id].n <= T) {
+        cuts.push_back(id);
+        return;
+    }
+    pcuts(v, v[id].l, T, cuts);
+    pcuts(v, v[id].r, T, cuts);
+}
+
+void pcollect(const std::vector<PNode> &v, int id, std::vector<int> &leaves,
+              std::vector<int> &internals)
+{
+    if (v[id].l < 0) {
+        leaves.push_back(id);
+        return;
+    }
+    pcollect(v, v[id].l, leaves, internals);
+    pcollect(v, v[id].r, leaves, internals);
+    internals.push_back(id);
+}
+
+int ptop(const std::vector<PNode> &v, int id, const std::vector<int> &cut_index,
+         std::vector<int> &top_nodes, std::vector<int> &top_h)
+{
+    // returns the height above the cut level; records top internals
+    if (cut_index[id] >= 0) return 0;
+    const int hl = ptop(v, v[id].l, cut_index, top_nodes, top_h);
+    const int hr = ptop(v, v[id].r, cut_index, top_nodes, top_h);
+    top_nodes.push_back(id);
+    top_h.push_back(1 + std::max(hl, hr));
+    return 1 + std::max(hl, hr);
+}
+
+int ensure_tree(evd_ctx *ctx, long long M, int cuts_target)
+{
+    TreePlan &tp = ctx->tree;
+    if (tp.M == M && tp.cuts_target == cuts_target) return EVD_OK;
+    if (M < 1 || M > (1ll << 30)) return fail(ctx, EVD_ERR_ARG, "image size %lld unsupported", M);
+    std::vector<PNode> v;
+    v.reserve((size_t)(2 * (M / 64 + 2)));
+    pbuild(v, 0, M);
+    long long T = std::max<long long>(128, (M + cuts_target - 1) / cuts_target);
+    std::vector<int> cuts;
+    std::vector<int> cut_index;
+    // find a cut threshold whose subtrees and top fit the per-block scratch
+    while (true) {
+        cuts.clear();
+        pcuts(v, 0, T, cuts);
+        long long worst = 0;
+        for (int c : cuts) worst = std::max<long long>(worst, 2 * (v[c].n / 64 + 1));
+        if (worst <= kCutSmem && 2 * (long long)cuts.size() <= kCutSmem) break;
+        if (worst > kCutSmem) {
+            if (2 * (long long)cuts.size() > kCutSmem)
+                return fail(ctx, EVD_ERR_ARG, "image size %lld too large for the reduction plan", M);
+            T = T * 3 / 4;  // never hit for practical sizes; keeps subtrees small
+            if (T < 128) return fail(ctx, EVD_ERR_ARG, "reduction plan failed for M=%lld", M);
+        } else {
+            T *= 2;
+        }
+    }
+    cut_index.assign(v.size(), -1);
+    for (size_t c = 0; c < cuts.size(); c++) cut_index[cuts[c]] = (int)c;
+
+    const int C = (int)cuts.size();
+    std::vector<int2> leaves;
+    std::vector<int> cut_leaf0{0}, cut_trip0{0}, cut_lvl((size_t)C * (kMaxLevels + 1), 0),
+        cut_nlev(C, 0);
+    std::vector<int4> trip;
+    for (int c = 0; c < C; c++) {
+        std::vector<int> lv, in;
+        pcollect(v, cuts[c], lv, in);
+        // local indices: leaves in order, internals sorted by height
+        std::stable_sort(in.begin(), in.end(), [&](int a, int b) { return v[a].h < v[b].h; });
+        auto find_local = [&](int node) -> int {
+            for (size_t i = 0; i < lv.size(); i++)
+                if (lv[i] == node) return (int)i;
+            for (size_t i = 0; i < in.size(); i++)
+                if (in[i] == node) return (int)(lv.size() + i);
+            return -1;
+        };
+        for (int id : lv) leaves.push_back(make_int2((int)v[id].off, (int)v[id].n));
+        int lvl = 0, level_h = 0;
+        int *L = &cut_lvl[(size_t)c * (kMaxLevels + 1)];
+        for (size_t i = 0; i < in.size(); i++) {
+            const int id = in[i];
+            const int rel = v[id].h;  // height above the leaves
+            if (i == 0 || rel != level_h) {
+                if (i > 0) lvl++;
+                if (lvl >= kMaxLevels) return fail(ctx, EVD_ERR_ARG, "tree too deep");
+                L[lvl] = (int)i;
+                level_h = rel;
+            }
+            trip.push_back(make_int4((int)(lv.size() + i), find_local(v[id].l),
+                                     find_local(v[id].r), 0));
+        }
+        const int nlev = in.empty() ? 0 : lvl + 1;
+        L[nlev] = (int)in.size();
+        cut_nlev[c] = nlev;
+        cut_leaf0.push_back((int)leaves.size());
+        cut_trip0.push_back((int)trip.size());
+    }
+    // top of the tree above the cuts
+    std::vector<int> top_nodes, top_h;
+    std::vector<int4> top;
+    std::vector<int> top_lvl;
+    int top_root = 0, top_levels = 0;
+    if (C > 1) {
+        ptop(v, 0, cut_index, top_nodes, top_h);
+        std::vector<int> order(top_nodes.size());
+        for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int a, int b) { return top_h[a] < top_h[b]; });
+        std::vector<int> top_index(v.size(), -1);
+        for (int c = 0; c < C; c++) top_index[cuts[c]] = c;
+        for (size_t i = 0; i < order.size(); i++) top_index[top_nodes[order[i]]] = C + (int)i;
+        int cur_h = -1;
+        for (size_t i = 0; i < order.size(); i++) {
+            const int id = top_nodes[order[i]];
+            if (top_h[order[i]] != cur_h) {
+                top_lvl.push_back((int)i);
+                cur_h = top_h[order[i]];
+            }
+            top.push_back(make_int4(top_index[id], top_index[v[id].l], top_index[v[id].r], 0));
+        }
+        top_levels = (int)top_lvl.size();
+        top_lvl.push_back((int)order.size());
+        top_root = top_index[0];
+        if (C + (long long)order.size() > kCutSmem) return fail(ctx, EVD_ERR_ARG, "top too large");
+    } else {
+        top_lvl.push_back(0);
+    }
+    CU(tp.leaves.ensure(leaves.size()));
+    CU(tp.cut_leaf0.ensure(cut_leaf0.size()));
+    CU(tp.cut_trip0.ensure(cut_trip0.size()));
+    CU(tp.cut_lvl.ensure(cut_lvl.size()));
+    CU(tp.cut_nlev.ensure(cut_nlev.size()));
+    CU(tp.trip.ensure(std::max<size_t>(trip.size(), 1)));
+    CU(tp.top.ensure(std::max<size_t>(top.size(), 1)));
+    CU(tp.top_lvl.ensure(top_lvl.size()));
+    CU(tp.cutval.ensure(C));
+    auto up = [&](void *dst, const void *src, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream)
+                     : cudaSuccess;
+    };
+    CU(up(tp.leaves.p, leaves.data(), leaves.size() * sizeof(int2)));
+    CU(up(tp.cut_leaf0.p, cut_leaf0.data(), cut_leaf0.size() * sizeof(int)));
+    CU(up(tp.cut_trip0.p, cut_trip0.data(), cut_trip0.size() * sizeof(int)));
+    CU(up(tp.cut_lvl.p, cut_lvl.data(), cut_lvl.size() * sizeof(int)));
+    CU(up(tp.cut_nlev.p, cut_nlev.data(), cut_nlev.size() * sizeof(int)));
+    CU(up(tp.trip.p, trip.data(), trip.size() * sizeof(int4)));
+    CU(up(tp.top.p, top.data(), top.size() * sizeof(int4)));
+    CU(up(tp.top_lvl.p, top_lvl.data(), top_lvl.size() * sizeof(int)));
+    CU(cudaStreamSynchronize(ctx->stream));  // host vectors die at return
+    TreeDev &d = tp.dev;
+    d.M = (int)M;
+    d.L = (int)leaves.size();
+    d.C = C;
+    d.leaves = tp.leaves.p;
+    d.cut_leaf0 = tp.cut_leaf0.p;
+    d.cut_trip0 = tp.cut_trip0.p;
+    d.cut_lvl = tp.cut_lvl.p;
+    d.cut_nlev = tp.cut_nlev.p;
+    d.trip = tp.trip.p;
+    d.top = tp.top.p;
+    d.top_lvl = tp.top_lvl.p;
+    d.top_levels = top_levels;
+    d.top_root = top_root;
+    d.cutval = tp.cutval.p;
+    tp.M = M;
+    tp.cuts_target = cuts_target;
+    return EVD_OK;
+}
+
+// pow through a volatile pointer so the compiler cannot fold pow(x, 2.0) to x*x:
+// CPython's float ** int calls libm pow(), which is not always x*x.
+double (*volatile g_pow)(double, double) = pow;
+
+void pow2_fill(long long m, long long n, double *out)
+{
+    const double dm = (double)m;
+    for (long long f = 0; f <= n; f++) out[f] = g_pow((double)f / dm, 2.0);
+}
+
+int ensure_pow2(evd_ctx *ctx, long long m, long long n)
+{
+    if (ctx->pow_m == m && ctx->pow_n >= n) return EVD_OK;
+    const long long want = std::max(n, 2 * std::max(ctx->pow_m == m ? ctx->pow_n : 0ll, 1024ll));
+    std::vector<double> h((size_t)want + 1);
+    pow2_fill(m, want, h.data());
+    CU(ctx->pow2.ensure((size_t)want + 1));
+    CU(cudaMemcpyAsync(ctx->pow2.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->pow_m = m;
+    ctx->pow_n = want;
+    return EVD_OK;
+}
+
+int need_events(evd_ctx *ctx)
+{
+    if (ctx->n < 0) return fail(ctx, EVD_ERR_STATE, "no events set (call evd_set_events first)");
+    return EVD_OK;
+}
+
+int check_den(evd_ctx *ctx, double nu, double tau, double *den)
+{
+    *den = 1.0 + nu * tau;  // geometry.py:72
+    if (!(*den > 0.0))
+        return fail(ctx, EVD_ERR_CHEIRALITY, "1 + nu*tau = %.17g <= 0 (nu=%.17g, tau=%.17g)",
+                    *den, nu, tau);
+    return EVD_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int evd_create(int device, evd_ctx **out)
+{
+    evd_ctx *ctx = nullptr;
+    if (!out) return fail(nullptr, EVD_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(nullptr, EVD_ERR_CUDA, "no CUDA device: %s",
+                    e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    if (device < 0 || device >= count)
+        return fail(nullptr, EVD_ERR_ARG, "device %d out of range (%d devices)", device, count);
+    ctx = new evd_ctx();
+    ctx->device = device;
+    CU(cudaSetDevice(device));
+    CU(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    ctx->stream = ctx->own;
+    CU(cudaEventCreate(&ctx->ev0));
+    CU(cudaEventCreate(&ctx->ev1));
+    CU(ctx->acc.ensure(8));
+    CU(ctx->dscratch.ensure(64));
+    *out = ctx;
+    return EVD_OK;
+}
+
+void evd_destroy(evd_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf<double> *b : {&ctx->xc, &ctx->yc, &ctx->t, &ctx->dscratch, &ctx->wx, &ctx->wy,
+                              &ctx->wt, &ctx->wxo, &ctx->wyo, &ctx->segs, &ctx->pow2})
+        b->release();
+    ctx->img.release();
+    ctx->seg_counts.release();
+    ctx->acc.release();
+    ctx->state.release();
+    ctx->frontier.release();
+    ctx->bar.release();
+    TreePlan &tp = ctx->tree;
+    tp.leaves.release();
+    tp.cut_leaf0.release();
+    tp.cut_trip0.release();
+    tp.cut_lvl.release();
+    tp.cut_nlev.release();
+    tp.top_lvl.release();
+    tp.trip.release();
+    tp.top.release();
+    tp.cutval.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+const char *evd_last_error(const evd_ctx *ctx)
+{
+    return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+int evd_set_stream(evd_ctx *ctx, void *cuda_stream)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own;
+    return EVD_OK;
+}
+
+int64_t evd_kernel_launches(const evd_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+int evd_device_sms(const evd_ctx *ctx) { return ctx ? ctx->sms : -1; }
+
+int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                   int32_t width, int32_t height, double tau)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (n < 0 || width < 1 || height < 1)
+        return fail(ctx, EVD_ERR_ARG, "bad window: n=%lld %dx%d", (long long)n, width, height);
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "batch duration tau must be positive");
+    if (n > 0 && (!x || !y || !t)) return fail(ctx, EVD_ERR_ARG, "NULL event array");
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->xc.ensure(n));
+    CU(ctx->yc.ensure(n));
+    CU(ctx->t.ensure(n));
+    if (n > 0) {
+        // raw x, y land in the centred buffers and are centred in place
+        CU(cudaMemcpyAsync(ctx->xc.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->yc.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->t.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        launch_center(ctx->xc.p, ctx->yc.p, n, width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p,
+                      ctx->stream);
+        LAUNCHED(1);
+    }
+    ctx->n = n;
+    ctx->W = width;
+    ctx->H = height;
+    ctx->tau = tau;
+    return EVD_OK;
+}
+
+int evd_radial_warp(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                    double nu, double tau, int32_t width, int32_t height, double *x_out,
+                    double *y_out)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    double den;
+    int rc = check_den(ctx, nu, tau, &den);
+    if (rc) return rc;
+    if (n <= 0) return EVD_OK;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->wx.ensure(n));
+    CU(ctx->wy.ensure(n));
+    CU(ctx->wt.ensure(n));
+    CU(ctx->wxo.ensure(n));
+    CU(ctx->wyo.ensure(n));
+    CU(cudaMemcpyAsync(ctx->wx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->wy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->wt.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const double cx = width / 2.0, cy = height / 2.0;
+    launch_center(ctx->wx.p, ctx->wy.p, n, cx, cy, ctx->wx.p, ctx->wy.p, ctx->stream);
+    launch_warp(ctx->wx.p, ctx->wy.p, ctx->wt.p, n, nu, den, cx, cy, ctx->wxo.p, ctx->wyo.p,
+                ctx->stream);
+    LAUNCHED(2);
+    CU(cudaMemcpyAsync(x_out, ctx->wxo.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(y_out, ctx->wyo.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EVD_OK;
+}
+
+int evd_warp_scale(evd_ctx *ctx, const double *t, int64_t n, double nu, double tau,
+                   double *s_out)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    double den;
+    int rc = check_den(ctx, nu, tau, &den);
+    if (rc) return rc;
+    if (n <= 0) return EVD_OK;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->wt.ensure(n));
+    CU(ctx->wxo.ensure(n));
+    CU(cudaMemcpyAsync(ctx->wt.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    launch_scale(ctx->wt.p, n, nu, den, ctx->wxo.p, ctx->stream);
+    LAUNCHED(1);
+    CU(cudaMemcpyAsync(s_out, ctx->wxo.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EVD_OK;
+}
+
+int evd_point_images(evd_ctx *ctx, const double *nu, int32_t k, int64_t *in_image,
+                     double *contrast, uint32_t *counts)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    const long long M = (long long)ctx->W * ctx->H;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->img.ensure(3 * M));
+    CU(ctx->acc.ensure(8));
+    if (contrast && (rc = ensure_tree(ctx, M, ctx->sms))) return rc;
+    const double cx = ctx->W / 2.0, cy = ctx->H / 2.0;
+    for (int j = 0; j < k; j++) {
+        double den;
+        if ((rc = check_den(ctx, nu[j], ctx->tau, &den))) return rc;
+        CU(cudaMemsetAsync(ctx->img.p, 0, M * sizeof(unsigned int), ctx->stream));
+        CU(cudaMemsetAsync(ctx->acc.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+        launch_point_image(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, nu[j], den, cx, cy, ctx->W,
+                           ctx->H, ctx->img.p, ctx->acc.p, ctx->stream);
+        LAUNCHED(1);
+        if (contrast) {
+            launch_contrast_u32(ctx->img.p, ctx->acc.p, ctx->tree.dev, ctx->dscratch.p,
+                                ctx->stream);
+            LAUNCHED(2);
+            CU(cudaMemcpyAsync(contrast + j, ctx->dscratch.p, sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        unsigned long long hacc = 0;
+        CU(cudaMemcpyAsync(&hacc, ctx->acc.p, sizeof hacc, cudaMemcpyDeviceToHost, ctx->stream));
+        if (counts)
+            CU(cudaMemcpyAsync(counts + (size_t)j * M, ctx->img.p, M * sizeof(unsigned int),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (in_image) in_image[j] = (int64_t)hacc;
+    }
+    return EVD_OK;
+}
+
+int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
+                     uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks, uint32_t *counts)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    const long long M = (long long)ctx->W * ctx->H;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->img.ensure(3 * M));
+    CU(ctx->acc.ensure(8));
+    const double cx = ctx->W / 2.0, cy = ctx->H / 2.0;
+    for (int j = 0; j < k; j++) {
+        if (lo[j] > hi[j]) return fail(ctx, EVD_ERR_ARG, "empty interval [%.17g, %.17g]", lo[j], hi[j]);
+        double dl, dh;
+        if ((rc = check_den(ctx, lo[j], ctx->tau, &dl))) return rc;
+        if ((rc = check_den(ctx, hi[j], ctx->tau, &dh))) return rc;
+        CU(cudaMemsetAsync(ctx->img.p, 0, M * sizeof(unsigned int), ctx->stream));
+        CU(cudaMemsetAsync(ctx->acc.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+        launch_bound_image(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, lo[j], dl, hi[j], dh, cx, cy,
+                           ctx->W, ctx->H, ctx->img.p, ctx->acc.p, ctx->stream);
+        launch_image_sums(ctx->img.p, M, ctx->acc.p + 2, ctx->stream);
+        LAUNCHED(2);
+        unsigned long long h[4];
+        CU(cudaMemcpyAsync(h, ctx->acc.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        if (counts)
+            CU(cudaMemcpyAsync(counts + (size_t)j * M, ctx->img.p, M * sizeof(unsigned int),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (h[1] != h[2])
+            return fail(ctx, EVD_ERR_CUDA, "internal: marks %llu != image sum %llu", h[1], h[2]);
+        if (fully_inside) fully_inside[j] = (int64_t)h[0];
+        if (marks) marks[j] = h[2];
+        if (s_bar) s_bar[j] = h[3];
+    }
+    return EVD_OK;
+}
+
+int evd_image_contrast(evd_ctx *ctx, const double *counts, int64_t m, int64_t in_image,
+                       double *contrast)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (m < 1) return fail(ctx, EVD_ERR_ARG, "image must have at least one pixel");
+    CU(cudaSetDevice(ctx->device));
+    int rc = ensure_tree(ctx, m, ctx->sms);
+    if (rc) return rc;
+    CU(ctx->wx.ensure(m));
+    CU(cudaMemcpyAsync(ctx->wx.p, counts, m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const double mu = (double)in_image / (double)m;  // EventImage.mean (contrast.py:35-36)
+    launch_contrast_f64(ctx->wx.p, mu, ctx->tree.dev, ctx->dscratch.p, ctx->stream);
+    LAUNCHED(2);
+    CU(cudaMemcpyAsync(contrast, ctx->dscratch.p, sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EVD_OK;
+}
+
+int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t width,
+                           int32_t height, uint32_t *counts)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (width < 1 || height < 1 || k < 0) return fail(ctx, EVD_ERR_ARG, "bad raster request");
+    if (k == 0) return EVD_OK;
+    const size_t M = (size_t)width * height;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->segs.ensure(4 * (size_t)k));
+    CU(ctx->seg_counts.ensure(M * k));
+    CU(cudaMemcpyAsync(ctx->segs.p, segs, 4 * k * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemsetAsync(ctx->seg_counts.p, 0, M * k * sizeof(unsigned int), ctx->stream));
+    launch_raster_segments(ctx->segs.p, k, width, height, ctx->seg_counts.p, ctx->stream);
+    LAUNCHED(1);
+    CU(cudaMemcpyAsync(counts, ctx->seg_counts.p, M * k * sizeof(unsigned int),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EVD_OK;
+}
+
+int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !res) return fail(ctx, EVD_ERR_ARG, "params/result is NULL");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    memset(res, 0, sizeof *res);
+    if (ctx->n == 0) return fail(ctx, EVD_ERR_NO_EVENTS, "no events in batch");
+    if (!(params->gamma > 0.0)) return fail(ctx, EVD_ERR_ARG, "gamma must be positive");
+    const double tau = ctx->tau, eps = params->epsilon;
+    if (!(eps >= 0.0 && eps < 1.0)) return fail(ctx, EVD_ERR_ARG, "epsilon must be in [0, 1)");
+    // velocity_domain (geometry.py:61-67) and the first warps the reference makes
+    const double lo0 = -(1.0 - eps) / tau, hi0 = 0.0, c0 = 0.5 * (lo0 + hi0);
+    double den_c, den_lo, den_hi;
+    if ((rc = check_den(ctx, c0, tau, &den_c))) return rc;    // contrast_at(center), solver.py:93
+    if ((rc = check_den(ctx, lo0, tau, &den_lo))) return rc;  // bound_terms(domain), solver.py:97
+    if ((rc = check_den(ctx, hi0, tau, &den_hi))) return rc;
+    const long long M = (long long)ctx->W * ctx->H;
+    CU(cudaSetDevice(ctx->device));
+    if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
+    const int blocks = ctx->solve_blocks;
+    if ((rc = ensure_tree(ctx, M, blocks))) return rc;
+    if ((rc = ensure_pow2(ctx, M, ctx->n))) return rc;
+    CU(ctx->img.ensure(3 * M));
+    CU(ctx->state.ensure(1));
+    CU(ctx->bar.ensure(1));
+    long long cap = (long long)ctx->frontier.cap;
+    if (cap < 4096) cap = 4096;
+    const long long need = params->max_iterations + 2;
+    if (need > 0 && need < cap) cap = need;
+    while (true) {
+        CU(ctx->frontier.ensure((size_t)cap));
+        SolveState st{};
+        st.lo = lo0;
+        st.hi = hi0;
+        st.c = c0;
+        st.den_lo = den_lo;
+        st.den_c = den_c;
+        st.den_hi = den_hi;
+        st.mode = kModeRoot;
+        st.bound_gap = 0.0;
+        CU(cudaMemcpyAsync(ctx->state.p, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemsetAsync(ctx->bar.p, 0, sizeof(GridBar), ctx->stream));
+        CU(cudaMemsetAsync(ctx->img.p, 0, 3 * M * sizeof(unsigned int), ctx->stream));
+        SolveArgs a{};
+        a.xc = ctx->xc.p;
+        a.yc = ctx->yc.p;
+        a.t = ctx->t.p;
+        a.n = ctx->n;
+        a.W = ctx->W;
+        a.H = ctx->H;
+        a.cx = ctx->W / 2.0;
+        a.cy = ctx->H / 2.0;
+        a.tau = tau;
+        a.P = ctx->img.p;
+        a.A = ctx->img.p + M;
+        a.B = ctx->img.p + 2 * M;
+        a.tree = ctx->tree.dev;
+        a.pow2 = ctx->pow2.p;
+        a.gamma = params->gamma;
+        a.min_width = params->min_interval_width;
+        a.max_iter = params->max_iterations;
+        a.st = ctx->state.p;
+        a.fr = ctx->frontier.p;
+        a.fr_cap = (long long)ctx->frontier.cap;
+        a.bar = ctx->bar.p;
+        CU(cudaEventRecord(ctx->ev0, ctx->stream));
+        CU(launch_solve(a, blocks, ctx->stream));
+        LAUNCHED(1);
+        CU(cudaEventRecord(ctx->ev1, ctx->stream));
+        CU(cudaMemcpyAsync(&st, ctx->state.p, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (st.status == kStatusCapacity) {
+            cap *= 8;
+            continue;
+        }
+        res->nu = st.nu_hat;
+        res->contrast = st.c_hat;
+        res->bound_gap = st.bound_gap;
+        res->iterations = st.iterations;
+        res->bound_evals = st.bound_evals;
+        res->point_evals = st.point_evals;
+        res->max_frontier = st.max_fr;
+        res->device_ms = ms;
+        if (st.status == kStatusIterLimit)
+            return fail(ctx, EVD_ERR_ITER_LIMIT,
+                        "iteration limit reached after %lld iterations (best nu=%.17g, contrast=%.17g)",
+                        st.iterations, st.nu_hat, st.c_hat);
+        return EVD_OK;
+    }
+}
+
+int evd_pow2_table(int64_t m, int64_t n, double *out)
+{
+    if (m < 1 || n < 0 || !out) return fail(nullptr, EVD_ERR_ARG, "bad pow2 table request");
+    pow2_fill(m, n, out);
+    return EVD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// evd_internal.h -- structures shared by the host API (evd_api.cu) and the
+// kernels (evd_kernels.cu).  Not part of the public C ABI (include/evd.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace evd {
+
+constexpr int kMaxLevels = 32;    // heights of a numpy pairwise tree (log2(M/64)+1)
+constexpr int kCutSmem = 4096;    // doubles of per-block scratch for a cut subtree / top
+
+// Fixed numpy pairwise-summation tree over M pixels, split into C "cut"
+// subtrees (evaluated one per block in parallel) and a top part (one block).
+struct TreeDev {
+    int M, L, C;
+    const int2 *leaves;      // [L] (offset, n), left to right
+    const int *cut_leaf0;    // [C+1] leaf range of each cut
+    const int *cut_trip0;    // [C+1] triple range of each cut
+    const int *cut_lvl;      // [C*(kMaxLevels+1)] per-cut level starts (relative)
+    const int *cut_nlev;     // [C]
+    const int4 *trip;        // (dst, l, r, -) local indices, sorted by height
+    const int4 *top;         // (dst, l, r, -) in top index space (cuts 0..C-1, then internals)
+    const int *top_lvl;      // [top_levels+1]
+    int top_levels;
+    int top_root;
+    double *cutval;          // [C] scratch
+};
+
+struct FrontierEntry {
+    double bound;
+    long long counter;
+    double lo, hi;
+};
+
+enum SolveMode : int { kModeRoot = 0, kModeNode = 1 };
+enum SolveStatus : int { kStatusOk = 0, kStatusIterLimit = 1, kStatusCapacity = 2 };
+
+// Device-resident BnB state (one per context); host reads it back at the end.
+struct SolveState {
+    // node under evaluation
+    double lo, hi, c, den_lo, den_c, den_hi;
+    int mode, done;
+    // per-iteration accumulators: 0 in_image, 1 fully_inside A, 2 fully_inside B,
+    // 3 S_bar A, 4 S_bar B, 5 marks A, 6 marks B
+    unsigned long long acc[8];
+    // incumbent and diagnostics
+    double nu_hat, c_hat, bound_gap;
+    long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
+    int status, pad;
+};
+
+struct SolveArgs {
+    const double *xc, *yc, *t;
+    long long n;
+    int W, H;
+    double cx, cy, tau;
+    unsigned int *P, *A, *B;  // point image, two child segment images (u32, zeroed)
+    TreeDev tree;
+    const double *pow2;       // pow(fi / M, 2.0) via host libm, fi in [0, n]
+    double gamma, min_width;
+    long long max_iter;
+    SolveState *st;
+    FrontierEntry *fr;
+    long long fr_cap;
+    void *bar;                // GridBar
+};
+
+// ---- kernel launchers (evd_kernels.cu); all asynchronous on `s` ----
+void launch_center(const double *x, const double *y, long long n, double cx, double cy,
+                   double *xc, double *yc, cudaStream_t s);
+void launch_warp(const double *xc, const double *yc, const double *t, long long n, double nu,
+                 double den, double cx, double cy, double *xo, double *yo, cudaStream_t s);
+void launch_scale(const double *t, long long n, double nu, double den, double *s, cudaStream_t st);
+void launch_point_image(const double *xc, const double *yc, const double *t, long long n,
+                        double nu, double den, double cx, double cy, int W, int H,
+                        unsigned int *img, unsigned long long *acc, cudaStream_t s);
+void launch_bound_image(const double *xc, const double *yc, const double *t, long long n,
+                        double lo, double den_lo, double hi, double den_hi, double cx, double cy,
+                        int W, int H, unsigned int *img, unsigned long long *acc,
+                        cudaStream_t s);
+void launch_image_sums(const unsigned int *img, long long m, unsigned long long *acc,
+                       cudaStream_t s);
+void launch_contrast_u32(const unsigned int *img, const unsigned long long *in_image,
+                         const TreeDev &tree, double *out, cudaStream_t s);
+void launch_contrast_f64(const double *img, double mu, const TreeDev &tree, double *out,
+                         cudaStream_t s);
+void launch_raster_segments(const double *segs, int k, int W, int H, unsigned int *counts,
+                            cudaStream_t s);
+int solve_grid_blocks(int device);
+int solve_block_threads();
+cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
+
+}  // namespace evd

@@ -1,0 +1,257 @@
+"""Parity of the CUDA path (through the C ABI) with the reference (GPU).
+
+Bar: bit-exact for every integer image, count and bound, and for every
+float64 contrast / c_bar bit pattern; BnbResult fields identical (runtime
+excepted).  Checked against fixtures made by the reference itself
+(tests/golden/) and, on fresh seeded inputs, against the pinned CPU oracle.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, f64, golden_segment_sets, random_batch
+from oracle import oracle as orc
+import paper_2209_13168_b200 as evd
+from paper_2209_13168_b200 import _lib, contrast as con, solver as sol, synth
+from paper_2209_13168_b200.events import EventBatch, SensorGeometry
+from paper_2209_13168_b200.geometry import VelocityInterval, velocity_domain
+
+pytestmark = pytest.mark.gpu
+
+
+def test_native_library_is_loaded():
+    ctx = _lib.context()
+    assert ctx.sms > 0
+    with open("/proc/self/maps") as fh:
+        assert _lib.LIB_PATH in fh.read()
+
+
+# ------------------------------------------------------------------ raster
+def test_segments_match_reference(seg_golden):
+    by_dims = {}
+    for seg, dims, cells in golden_segment_sets(seg_golden):
+        by_dims.setdefault(dims, []).append((seg, cells))
+    bad = 0
+    for (w, h), items in by_dims.items():
+        got = con.rasterize_segments([s for s, _ in items], SensorGeometry(w, h))
+        bad += sum(g != c for g, (_, c) in zip(got, items))
+    assert bad == 0
+
+
+def test_fresh_adversarial_segments_vs_oracle():
+    r = np.random.default_rng(99)
+    g = SensorGeometry(32, 24)
+    segs = np.concatenate([
+        r.uniform(-4, 36, (6000, 4)),
+        r.integers(-2, 35, (3000, 4)).astype(float),
+        np.round(r.uniform(-2, 34, (2000, 4)) * 2) / 2,
+    ])
+    got = con.rasterize_segments(segs, g)
+    bad = sum(got[j] != orc.rasterize_segment(s[:2], s[2:], 32, 24) for j, s in enumerate(segs))
+    assert bad == 0
+
+
+def test_reference_raster_examples():
+    g = SensorGeometry(8, 8)
+    assert evd.rasterize_segment((2.5, 2.5), (2.5, 2.5), g) == {(2, 2)}
+    assert evd.rasterize_segment((0.5, 0.5), (2.5, 0.5), g) == {(0, 0), (1, 0), (2, 0)}
+    assert evd.rasterize_segment((-5.0, -5.0), (-1.0, -2.0), g) == set()
+    px = evd.rasterize_segment((3.0, 3.0), (5.0, 5.0), g)
+    assert {(3, 3), (4, 4), (3, 4), (4, 3)} <= px
+
+
+# ------------------------------------------------------------------ images
+def test_point_images_and_contrast_bits(img_golden):
+    for meta, batch, arr in img_golden:
+        for j, p in enumerate(meta["points"]):
+            nu = f64(p["nu"])
+            img = evd.accumulate_image(batch, nu)
+            assert np.array_equal(img.counts, arr[f"point{j}"].astype(np.float64)), (meta["name"], j)
+            assert img.in_image_events == p["in_image"]
+            assert evd.contrast_at(batch, nu) == f64(p["contrast"])
+            assert evd.image_contrast(img) == f64(p["contrast"])
+            assert evd.image_contrast_expanded(img) == f64(p["contrast_expanded"])
+
+
+def test_bound_images_and_terms_bits(img_golden):
+    for meta, batch, arr in img_golden:
+        for j, b in enumerate(meta["bounds"]):
+            iv = VelocityInterval(f64(b["lo"]), f64(b["hi"]))
+            ub = evd.upper_bound_image(batch, iv)
+            assert np.array_equal(ub.counts, arr[f"bound{j}"].astype(np.float64)), (meta["name"], j)
+            assert ub.in_image_events == b["marks"]
+            bt = evd.bound_terms(batch, iv)
+            assert (bt.s_bar, bt.mu_lower, bt.c_bar) == (
+                f64(b["s_bar"]), f64(b["mu_lower"]), f64(b["c_bar"])), (meta["name"], j)
+
+
+def test_batched_bounds_equal_single_calls(img_golden):
+    meta, batch, arr = img_golden[0]
+    lo = [f64(b["lo"]) for b in meta["bounds"]]
+    hi = [f64(b["hi"]) for b in meta["bounds"]]
+    s, fi, marks, counts = con.bound_terms_many(batch, lo, hi, images=True)
+    for j, b in enumerate(meta["bounds"]):
+        assert np.array_equal(counts[j], arr[f"bound{j}"])
+        assert int(fi[j]) == b["fully_inside"] and int(marks[j]) == b["marks"]
+        assert float(s[j]) == f64(b["s_bar"])
+
+
+def test_full_size_bound_images_vs_oracle():
+    """Whole (batch, interval) images at config-1 size, incl. the near-singular root."""
+    b = synth.config_window(1)
+    dom = velocity_domain(b.tau)
+    ivs = [(dom.lo, dom.hi), dom.split()[0], (dom.lo, dom.lo + 1e-3), (-0.45, -0.35),
+           (-0.40001, -0.39999), (-0.4, -0.4), (-1.5, -1.2)]
+    ivs = [(iv.lo, iv.hi) if isinstance(iv, VelocityInterval) else iv for iv in ivs]
+    s, fi, marks, counts = con.bound_terms_many(b, [a for a, _ in ivs], [c for _, c in ivs],
+                                                images=True)
+    orc.THREADS = 8
+    try:
+        for j, (lo, hi) in enumerate(ivs):
+            oc, ofi = orc.bound_image(b, lo, hi)
+            assert np.array_equal(counts[j], oc), (lo, hi)
+            assert int(fi[j]) == ofi and int(marks[j]) == int(oc.sum())
+            assert int(s[j]) == int((oc.astype(np.uint64) ** 2).sum())
+    finally:
+        orc.THREADS = 1
+
+
+def test_warp_bits_vs_oracle():
+    b = synth.config_window(1)
+    for nu in (0.0, -0.4, -1.999998, -1e-300, -0.7):
+        x, y = evd.warp_batch(b, nu)
+        ox, oy = orc.warp(b.x, b.y, b.t, nu, b.tau, 240, 180)
+        assert np.array_equal(x, ox) and np.array_equal(y, oy)
+    s = evd.warp_scale(b.t, -0.4, 0.5)
+    assert np.array_equal(s, (1.0 + -0.4 * b.t) / (1.0 + -0.4 * 0.5))
+
+
+# ------------------------------------------------------------------ solver
+def _same(r, ref):
+    return (r.nu, r.contrast, r.bound_gap, r.iterations) == (
+        f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
+
+
+def test_bnb_small_windows(bnb_golden):
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        r = evd.maximise_contrast_bnb(batch, evd.SolverParams())
+        assert _same(r, w["result"]), w["result"]
+
+
+def test_bnb_trace_nodes(bnb_golden):
+    """Every node the reference evaluated: centre contrast and both child c_bar bits."""
+    meta, windows = bnb_golden
+    for w, batch in windows[:4]:
+        m = batch.geometry.n_pixels
+        nodes = [n for n in w["trace"] if n["kind"] == "node"]
+        if not nodes:
+            continue
+        los = [f64(n["lo"]) for n in nodes]
+        his = [f64(n["hi"]) for n in nodes]
+        cs = [0.5 * (a + b) for a, b in zip(los, his)]
+        _, contrast, _ = con.point_terms(batch, cs)
+        s, fi, _, _ = con.bound_terms_many(batch, los + cs, cs + his)
+        k = len(nodes)
+        for j, n in enumerate(nodes):
+            assert contrast[j] == f64(n["c_center"])
+            for side, idx in ((0, j), (1, k + j)):
+                cb = con.assemble_bound(int(s[idx]), int(fi[idx]), m)
+                assert cb.c_bar == f64(n["children"][side]["c_bar"])
+
+
+@pytest.mark.parametrize("cfg", ["1", "2"])
+def test_bnb_configs(cfg):
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        ref = json.load(fh)["configs"][cfg]
+    b = synth.config_window(int(cfg))
+    assert b.n == ref["n"]
+    r, stats = sol.solve_window(b, evd.SolverParams())
+    assert _same(r, ref["result"])
+    assert stats.bound_evals == 1 + 2 * (r.iterations - 1) or stats.bound_evals <= 2 * r.iterations + 1
+
+
+def test_bnb_config3_if_golden():
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        ref = json.load(fh)["configs"].get("3")
+    if ref is None:
+        pytest.skip("config-3 golden not generated")
+    b = synth.config_window(3)
+    r = evd.maximise_contrast_bnb(b, evd.SolverParams())
+    assert _same(r, ref["result"])
+
+
+def test_sequence_windows(bnb_golden):
+    meta, _ = bnb_golden
+    for s in meta["sequence"]:
+        b = synth.sequence_window(s["k"])
+        assert b.n == s["n"]
+        assert _same(evd.maximise_contrast_bnb(b, evd.SolverParams()), s["result"])
+
+
+def test_grid_search(bnb_golden):
+    meta, windows = bnb_golden
+    for g in meta["grid"]:
+        nu, c = evd.grid_search_oracle(windows[g["window"]][1], evd.SolverParams(), g["n_points"])
+        assert (nu, c) == (f64(g["nu"]), f64(g["c"]))
+
+
+def test_iteration_limit(bnb_golden):
+    meta, windows = bnb_golden
+    lim = meta["iteration_limit"]
+    with pytest.raises(evd.IterationLimitError) as err:
+        evd.maximise_contrast_bnb(windows[lim["window"]][1],
+                                  evd.SolverParams(max_iterations=lim["max_iterations"]))
+    e = err.value
+    assert (e.nu, e.contrast, e.iterations) == (f64(lim["nu"]), f64(lim["contrast"]),
+                                                lim["iterations"])
+
+
+def test_errors():
+    g = SensorGeometry(8, 8)
+    empty = EventBatch(np.empty(0), np.empty(0), np.empty(0), 0.5, g)
+    with pytest.raises(evd.NoEventsError):
+        evd.maximise_contrast_bnb(empty, evd.SolverParams())
+    one = EventBatch(np.array([3.0]), np.array([3.0]), np.array([0.1]), 0.5, g)
+    with pytest.raises(evd.CheiralityError):
+        evd.maximise_contrast_bnb(one, evd.SolverParams(epsilon=0.0))
+    with pytest.raises(evd.CheiralityError):
+        evd.radial_warp(1.0, 1.0, 0.0, nu=-2.0, tau=0.5, geometry=SensorGeometry(100, 100))
+    with pytest.raises(evd.CheiralityError):
+        evd.bound_terms(one, VelocityInterval(-2.5, 0.0))
+
+
+def test_stream_driver_gaps(rng):
+    n = 400
+    t = np.sort(np.concatenate([rng.uniform(0, 0.5, n), rng.uniform(2.5, 3.0, n)]))
+    s = evd.EventStream(rng.uniform(0, 64, 2 * n), rng.uniform(0, 64, 2 * n), t,
+                        np.ones(2 * n, dtype=np.int8), SensorGeometry(64, 64))
+    samples = evd.estimate_stream_divergence(evd.batch_stream(s, 0.5), evd.SolverParams())
+    assert [x.t for x in samples] == [0.5, 3.0]
+    for x, b in zip(samples, [b for b in evd.batch_stream(s, 0.5) if b.n]):
+        r = orc.maximise_contrast_bnb(b)
+        assert (x.contrast, x.iterations) == (r.contrast, r.iterations)
+        assert x.divergence == evd.divergence_from_velocity(r.nu, 0.5)
+
+
+# ------------------------------------------------------------------ properties at full size
+@pytest.mark.parametrize("cfg", [2])
+def test_bound_validity_properties_full_size(cfg):
+    """Size-independent properties at BASELINE sizes: H_bar >= H for nu in the
+    interval, monotone refinement, singleton equality, marks == sum(H_bar)."""
+    b = synth.config_window(cfg)
+    r = np.random.default_rng(cfg)
+    dom = velocity_domain(b.tau)
+    for _ in range(4):
+        lo, hi = np.sort(r.uniform(dom.lo, dom.hi, 2))
+        ilo, ihi = np.sort(r.uniform(lo, hi, 2))
+        nu = float(r.uniform(ilo, ihi))
+        _, fi, marks, ims = con.bound_terms_many(b, [lo, ilo, nu], [hi, ihi, nu], images=True)
+        ins, _, pim = con.point_terms(b, [nu], images=True, with_contrast=False)
+        assert (ims[1] <= ims[0]).all() and (pim[0] <= ims[1]).all()
+        assert np.array_equal(ims[2], pim[0])
+        assert [int(ims[j].sum(dtype=np.uint64)) for j in range(3)] == [int(m) for m in marks]
+        assert fi[2] == ins[0]

@@ -1,0 +1,92 @@
+"""Pin the CPU oracle to fixtures produced by the reference itself (CPU only).
+
+The oracle (oracle/) is the checker of the CUDA path; before trusting it, it
+must reproduce every golden vector the reference generated
+(tests/golden/make_golden.py) bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import f64, golden_segment_sets
+from oracle import oracle as orc
+
+
+def test_segments_match_reference(seg_golden):
+    bad = 0
+    for seg, (w, h), cells in golden_segment_sets(seg_golden):
+        if orc.rasterize_segment(seg[:2], seg[2:], w, h) != cells:
+            bad += 1
+    assert bad == 0
+
+
+def test_point_images_and_contrast(img_golden):
+    for meta, batch, arr in img_golden:
+        for j, p in enumerate(meta["points"]):
+            counts, inside = orc.point_image(batch, f64(p["nu"]))
+            assert np.array_equal(counts, arr[f"point{j}"]), (meta["name"], j)
+            assert inside == p["in_image"]
+            assert orc.image_contrast(counts, inside) == f64(p["contrast"])
+
+
+def test_bound_images_and_terms(img_golden):
+    for meta, batch, arr in img_golden:
+        m = meta["width"] * meta["height"]
+        for j, b in enumerate(meta["bounds"]):
+            s_bar, mu_lower, c_bar, fi, counts = orc.bound_terms(batch, f64(b["lo"]), f64(b["hi"]))
+            assert np.array_equal(counts, arr[f"bound{j}"]), (meta["name"], j)
+            assert fi == b["fully_inside"]
+            assert int(counts.sum()) == b["marks"]
+            assert s_bar == f64(b["s_bar"]) and mu_lower == f64(b["mu_lower"])
+            assert c_bar == f64(b["c_bar"])
+            assert fi / m == f64(b["mu_lower"])
+
+
+def test_bnb_small_windows(bnb_golden):
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        r = orc.maximise_contrast_bnb(batch)
+        ref = w["result"]
+        assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (
+            f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
+
+
+def test_bnb_config1():
+    from paper_2209_13168_b200 import synth
+    import json, os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        ref = json.load(fh)["configs"]["1"]["result"]
+    orc.THREADS = 4
+    try:
+        r = orc.maximise_contrast_bnb(synth.config_window(1))
+    finally:
+        orc.THREADS = 1
+    assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (
+        f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
+
+
+def test_grid_search(bnb_golden):
+    meta, windows = bnb_golden
+    for g in meta["grid"]:
+        nu, c = orc.grid_search(windows[g["window"]][1], g["n_points"])
+        assert (nu, c) == (f64(g["nu"]), f64(g["c"]))
+
+
+@pytest.mark.parametrize("m", list(range(1, 140)) + [255, 256, 257, 1000, 43200, 89960])
+def test_pairwise_restatement_matches_numpy(m):
+    r = np.random.default_rng(m)
+    a = (r.integers(0, 9, m).astype(np.float64) - r.random()) ** 2
+    assert orc.pairwise_sum(a) == np.sum(a)
+
+
+def test_multithreaded_oracle_is_deterministic(img_golden):
+    meta, batch, arr = img_golden[3]
+    b = meta["bounds"][0]
+    c1, f1 = orc.bound_image(batch, f64(b["lo"]), f64(b["hi"]))
+    orc.THREADS = 5
+    try:
+        c5, f5 = orc.bound_image(batch, f64(b["lo"]), f64(b["hi"]))
+    finally:
+        orc.THREADS = 1
+    assert np.array_equal(c1, c5) and f1 == f5
