@@ -1,0 +1,285 @@
+"""Benchmark: single-window BnB divergence solves on B200 (BASELINE.json configs[1]).
+
+Workload (BASELINE.json configs[1], SURVEY.md §8(d) cfg 2): the 346x260
+DAVIS-sized synthetic ventral-descent window, 204,203 events (window 0 of the
+SimConfig(nu=-0.4, n_points=10000, seed=0) stream, regenerated bit-identically
+by paper_2209_13168_b200.synth), one reference-order best-first BnB solve per
+step (gamma=0.025, tau=0.5, epsilon=1e-6).
+
+  value  solves/s with the window resident in HBM; device time of each step
+         (CUDA events on the stream the persistent kernel runs on), L2 flushed
+         between steps (the 4.9 MB window would otherwise stay in the 126 MB L2)
+  e2e    the same metric through the public API maximise_contrast_bnb(batch)
+         with pinned host arrays: per step H2D of the window + solve + D2H of
+         the result, host wall clock
+  --impl reference
+         the reference algorithm's CPU implementation (the pinned oracle port,
+         oracle/, every host thread) on the same window and metric
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+(N>1: launch under torch.distributed.run; ranks solve independent windows.)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = {"workload": "cfg2: 346x260 window, 204203 events, single-window BnB solve",
+          "sensor": "346x260", "events": 204203, "gamma": 0.025, "tau": 0.5,
+          "l2": "flushed between steps (256 MiB write)"}
+METRIC = "divergence solves/sec"
+UNIT = "solves/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
+        mx = [int(s[1]) for s in self.samples if s[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_solve_sample(batch, threads):
+    from oracle import oracle as orc
+    orc.THREADS = threads
+    t0 = time.perf_counter()
+    r = orc.maximise_contrast_bnb(batch)
+    return time.perf_counter() - t0, r
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """The reference algorithm on the host cores (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2209_13168_b200 import synth
+    batch = synth.config_window(2)
+    threads = host_threads()
+    for _ in range(args.warmup):
+        cpu_solve_sample(batch, threads)
+    times = []
+    r = None
+    for _ in range(args.steps):
+        dt, r = cpu_solve_sample(batch, threads)
+        times.append(dt)
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": CONFIG,
+        "events_x_bound_evals_per_s": batch.n * r.bound_evals / (total / args.steps),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "one full cfg-2 BnB solve per step (96 iterations, 191 "
+                                   "bound evals), oracle/ C restatement, events split over "
+                                   f"{threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result": {"nu": r.nu, "contrast": r.contrast, "iterations": r.iterations},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, rank, world, local):
+    import torch
+    import paper_2209_13168_b200 as evd
+    from paper_2209_13168_b200 import _lib, solver as sol, synth
+    from paper_2209_13168_b200.contrast import load_window
+
+    torch.cuda.set_device(local)
+    _lib.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    batch = synth.config_window(2)
+    params = evd.SolverParams()
+    ctx = _lib.context(local)
+    stream = torch.cuda.current_stream()
+    ctx.lib.evd_set_stream(ctx.h, _lib._vp(stream.cuda_stream))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- value: resident window, device-timed steps
+    load_window(batch, ctx)
+    for _ in range(args.warmup):
+        res, _ = sol.solve_loaded(ctx, params)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kernel_ms = []
+    barrier()
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            res, _ = sol.solve_loaded(ctx, params)
+            ev[k][1].record(stream)
+            kernel_ms.append(res.device_ms)
+        barrier()
+    launches = ctx.launches - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_dev = dev_ms / 1e3
+    if world > 1:
+        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    value = world * args.steps / t_dev
+
+    # ---------------- e2e: public API, pinned host buffers, H2D + solve + D2H each step
+    pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(batch, k))).pin_memory()
+           for k in ("x", "y", "t")}
+    pbatch = evd.EventBatch(pin["x"].numpy(), pin["y"].numpy(), pin["t"].numpy(), batch.tau,
+                            batch.geometry)
+    for _ in range(args.warmup):
+        evd.maximise_contrast_bnb(pbatch, params)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # same L2 state as the device-timed leg
+        r = evd.maximise_contrast_bnb(pbatch, params)
+    barrier()
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = world * args.steps / t_e2e
+
+    if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                peaks = json.load(fh)
+        except Exception:
+            pass
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        # algorithmic bytes of k_solve: each node evaluation streams the window
+        # once (24 B/event: x, y, t); images are not algorithmic
+        alg_bytes = 24.0 * batch.n * res.point_evals
+        k_ms = statistics.mean(kernel_ms)
+        achieved = alg_bytes / (k_ms / 1e3) / 1e9
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            with open(tfile) as fh:
+                traffic = json.load(fh).get("k_solve_dram_bytes")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference simulator restated, bit-identical window)",
+            "config": dict(CONFIG, parallelism=f"windows x{world} (no data-path collective)"),
+            "events_x_bound_evals_per_s": world * batch.n * res.bound_evals * args.steps / t_dev,
+            "solve": {"nu": res.nu, "contrast": res.contrast, "bound_gap": res.bound_gap,
+                      "iterations": res.iterations, "bound_evals": res.bound_evals,
+                      "point_evals": res.point_evals, "max_frontier": res.max_frontier,
+                      "kernel_ms": k_ms},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n,
+                    "d2h_bytes_per_step": 200},  # SolveState read back (evd_internal.h)
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "kernel": "k_solve", "achieved": achieved,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": traffic,
+                         "note": "latency-bound sequential BnB: one grid-wide node step per "
+                                 "iteration; algorithmic bytes = 24 B x events x node evals"},
+        }
+        if world == 1 and not args.no_cpu:
+            threads = host_threads()
+            dt, r = cpu_solve_sample(batch, threads)
+            same = (r.nu, r.contrast, r.iterations) == (res.nu, res.contrast, res.iterations)
+            line["cpu_baseline"] = {
+                "value": 1.0 / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": "one full cfg-2 BnB solve (oracle/ C restatement of the reference, "
+                          f"events split over {threads} threads); identical result: {same}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_gpu(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -90,9 +90,11 @@ int evd_image_contrast(evd_ctx *ctx, const double *counts, int64_t m, int64_t in
                        double *contrast);
 
 /* rasterize_segment (contrast.py:206-222) for k segments (ax, ay, bx, by);
- * counts receives k uint32 (height, width) mark images (each mark 0/1). */
+ * counts receives k uint32 (height, width) mark images (each mark 0/1).
+ * chunk: crossings per sampling chunk (0 = the kernels' default); any value
+ * gives the same pixels -- exposed so tests can exercise chunk seams. */
 int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t width,
-                           int32_t height, uint32_t *counts);
+                           int32_t height, int32_t chunk, uint32_t *counts);
 
 /* ---- branch and bound (maximise_contrast_bnb, solver.py:79-123) -------- */
 typedef struct {
@@ -117,6 +119,16 @@ typedef struct {
  * persistent launch).  Returns EVD_ERR_ITER_LIMIT with the incumbent in *res
  * when max_iterations is reached. */
 int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res);
+
+/* Device timestamps (ns, %globaltimer) of the last evd_solve: out[0] = start,
+ * then for node evaluation i (0 = root): out[1+2i] = every event binned,
+ * out[2+2i] = every pixel reduced.  *n receives the number of valid entries. */
+int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n);
+
+/* Per-block timestamps of the first 128 node evaluations of the last
+ * evd_solve: out[(i*blocks + b)*4 + k], k = node start, events done, pixels
+ * done, step done (diagnostics). */
+int evd_solve_block_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int32_t *blocks);
 
 /* ---- helpers ----------------------------------------------------------- */
 /* out[f] = pow(f / m, 2.0) through the process's libm pow(), f = 0..n: the

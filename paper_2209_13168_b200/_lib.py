@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libevd.so")
+LIB_PATH = os.environ.get("EVD_LIB") or os.path.join(HERE, "libevd.so")
 
 EVD_OK, EVD_ERR_CUDA, EVD_ERR_ARG, EVD_ERR_NO_EVENTS = 0, 1, 2, 3
 EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
@@ -24,7 +24,7 @@ SYMBOLS = (
     "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
     "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
     "evd_point_images", "evd_bound_images", "evd_image_contrast", "evd_rasterize_segments",
-    "evd_solve", "evd_pow2_table",
+    "evd_solve", "evd_solve_trace", "evd_solve_block_trace", "evd_pow2_table",
 )
 
 
@@ -74,8 +74,10 @@ _SIGS = {
     "evd_point_images": (ctypes.c_int, [_vp, _d, _i32, _i64p, _d, _u32p]),
     "evd_bound_images": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p, _u32p]),
     "evd_image_contrast": (ctypes.c_int, [_vp, _d, _i64, _i64, _d]),
-    "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _u32p]),
+    "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _i32, _u32p]),
     "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
+    "evd_solve_trace": (ctypes.c_int, [_vp, _i64p, _i64, _i64p]),
+    "evd_solve_block_trace": (ctypes.c_int, [_vp, _i64p, _i64, ctypes.POINTER(_i32)]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
 }
 

@@ -151,8 +151,12 @@ def rasterize_segment(p0: tuple[float, float], p1: tuple[float, float],
     return rasterize_segments([(p0[0], p0[1], p1[0], p1[1])], geometry)[0]
 
 
-def rasterize_segments(segments, geometry: SensorGeometry) -> list[set[tuple[int, int]]]:
-    """Batched rasterize_segment: one device launch for all segments."""
+def rasterize_segments(segments, geometry: SensorGeometry, chunk: int = 0
+                       ) -> list[set[tuple[int, int]]]:
+    """Batched rasterize_segment: one device launch for all segments.
+
+    ``chunk`` sets how many crossings one sampling chunk holds (0: default);
+    the pixels do not depend on it."""
     segs = _lib.f64(np.asarray(segments, dtype=np.float64).reshape(-1, 4))
     k = segs.shape[0]
     if k == 0:
@@ -160,7 +164,8 @@ def rasterize_segments(segments, geometry: SensorGeometry) -> list[set[tuple[int
     counts = np.empty((k, geometry.height, geometry.width), dtype=np.uint32)
     ctx = _lib.context()
     rc = ctx.lib.evd_rasterize_segments(ctx.h, _lib.ptr(segs), k, geometry.width,
-                                        geometry.height, _lib.ptr(counts, _lib._u32p))
+                                        geometry.height, int(chunk),
+                                        _lib.ptr(counts, _lib._u32p))
     if rc:
         _raise(ctx, rc)
     if counts.max(initial=0) > 1:

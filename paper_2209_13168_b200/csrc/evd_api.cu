@@ -84,6 +84,8 @@ struct evd_ctx {
     DevBuf<SolveState> state;
     DevBuf<FrontierEntry> frontier;
     DevBuf<GridBar> bar;
+    DevBuf<long long> trace, btrace;
+    long long trace_n = 0;
     int solve_blocks = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
@@ -603,7 +605,7 @@ int evd_image_contrast(evd_ctx *ctx, const double *counts, int64_t m, int64_t in
 }
 
 int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t width,
-                           int32_t height, uint32_t *counts)
+                           int32_t height, int32_t chunk, uint32_t *counts)
 {
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (width < 1 || height < 1 || k < 0) return fail(ctx, EVD_ERR_ARG, "bad raster request");
@@ -615,7 +617,7 @@ int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t 
     CU(cudaMemcpyAsync(ctx->segs.p, segs, 4 * k * sizeof(double), cudaMemcpyHostToDevice,
                        ctx->stream));
     CU(cudaMemsetAsync(ctx->seg_counts.p, 0, M * k * sizeof(unsigned int), ctx->stream));
-    launch_raster_segments(ctx->segs.p, k, width, height, ctx->seg_counts.p, ctx->stream);
+    launch_raster_segments(ctx->segs.p, k, width, height, chunk, ctx->seg_counts.p, ctx->stream);
     LAUNCHED(1);
     CU(cudaMemcpyAsync(counts, ctx->seg_counts.p, M * k * sizeof(unsigned int),
                        cudaMemcpyDeviceToHost, ctx->stream));
@@ -649,6 +651,9 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
     CU(ctx->img.ensure(3 * M));
     CU(ctx->state.ensure(1));
     CU(ctx->bar.ensure(1));
+    CU(ctx->trace.ensure(1 + kTraceSlots * kTraceIters));
+    CU(ctx->btrace.ensure((size_t)kBTraceIters * kBTraceMaxBlocks * kBTraceSlots));
+        CU(cudaMemsetAsync(ctx->trace.p, 0, (1 + kTraceSlots * kTraceIters) * sizeof(long long), ctx->stream));
     long long cap = (long long)ctx->frontier.cap;
     if (cap < 4096) cap = 4096;
     const long long need = params->max_iterations + 2;
@@ -689,6 +694,9 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
         a.fr = ctx->frontier.p;
         a.fr_cap = (long long)ctx->frontier.cap;
         a.bar = ctx->bar.p;
+        a.trace = ctx->trace.p;
+        a.trace_iters = kTraceIters;
+        a.btrace = ctx->btrace.p;
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
         CU(launch_solve(a, blocks, ctx->stream));
         LAUNCHED(1);
@@ -709,12 +717,34 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
         res->point_evals = st.point_evals;
         res->max_frontier = st.max_fr;
         res->device_ms = ms;
+        ctx->trace_n = 1 + kTraceSlots * std::min<long long>(st.iterations + 1, kTraceIters);
         if (st.status == kStatusIterLimit)
             return fail(ctx, EVD_ERR_ITER_LIMIT,
                         "iteration limit reached after %lld iterations (best nu=%.17g, contrast=%.17g)",
                         st.iterations, st.nu_hat, st.c_hat);
         return EVD_OK;
     }
+}
+
+int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    const long long k = std::min<long long>(cap, ctx->trace_n);
+    if (n) *n = ctx->trace_n;
+    if (k > 0 && ctx->trace.p) {
+        CU(cudaMemcpy(out, ctx->trace.p, k * sizeof(long long), cudaMemcpyDeviceToHost));
+    }
+    return EVD_OK;
+}
+
+int evd_solve_block_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int32_t *blocks)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (blocks) *blocks = ctx->solve_blocks;
+    const long long k = std::min<long long>(cap, (long long)kBTraceIters * ctx->solve_blocks * kBTraceSlots);
+    if (k > 0 && ctx->btrace.p)
+        CU(cudaMemcpy(out, ctx->btrace.p, k * sizeof(long long), cudaMemcpyDeviceToHost));
+    return EVD_OK;
 }
 
 int evd_pow2_table(int64_t m, int64_t n, double *out)

@@ -50,86 +50,129 @@ __device__ __forceinline__ int fully_inside(double ax, double ay, double bx, dou
 
 // ---------------------------------------------------------------- supercover
 // Per-event dedup.  The reference marks each pixel at most once per event with
-// a stamp grid (contrast.py:89-91).  The device replaces it with a comparison
-// against the previous _mark_point call only, which is exact: the sample
-// parameters are visited in sorted order, x(s) = cx0 + s*ddx and y(s) are
-// monotone in s under round-to-nearest, and a pixel's closed square is an
-// axis-aligned box, so the calls that mark a given pixel form one contiguous
-// run.  A pixel already marked by this event was therefore marked by the
-// immediately preceding call.  (DESIGN.md "Exact dedup" has the full argument.)
+// a stamp grid (contrast.py:89-91).  The device compares against the previous
+// _mark_point call only, which is exact: the sample parameters are visited in
+// sorted order, x(s) = cx0 + s*ddx and y(s) = cy0 + s*ddy are monotone in s
+// under round-to-nearest, and a pixel's closed square is an axis-aligned box,
+// so the calls that mark a given pixel form one contiguous run -- a pixel
+// already marked by this event was marked by the immediately preceding call.
+// (DESIGN.md "Exact dedup" has the full argument.)
 struct Prev {
-    long long x0, x1, y0, y1;  // previous call's closed-square pixel range (inclusive)
+    int x0, x1, y0, y1;  // previous call's closed-square pixel range (inclusive)
 };
 
-template <class Sink>
-__device__ __forceinline__ void mark_point(double px, double py, int W, int H, Prev &prev,
-                                           Sink &sink)
+// Pixel range [x0, x1] x [y0, y1] of the closed unit squares containing (px, py)
+// (contrast.py:73-91).  Points reaching here come from a segment clipped to
+// the frame, so the ranges fit in int.
+__device__ __forceinline__ Prev point_range(double px, double py)
 {
-    // contrast.py:73-91: every pixel whose closed unit square contains (px, py)
     const double fx = floor(px), fy = floor(py);
-    const long long ix1 = (long long)fx, iy1 = (long long)fy;
-    const long long ix0 = (px == fx) ? ix1 - 1 : ix1;
-    const long long iy0 = (py == fy) ? iy1 - 1 : iy1;
-    for (long long ix = ix0; ix <= ix1; ix++) {
-        if (ix < 0 || ix >= W) continue;
-        const bool px_in = ix >= prev.x0 && ix <= prev.x1;
-        for (long long iy = iy0; iy <= iy1; iy++) {
-            if (iy < 0 || iy >= H) continue;
-            if (px_in && iy >= prev.y0 && iy <= prev.y1) continue;
+    const int ix1 = (int)fx, iy1 = (int)fy;
+    return {(px == fx) ? ix1 - 1 : ix1, ix1, (py == fy) ? iy1 - 1 : iy1, iy1};
+}
+
+template <class Sink>
+__device__ __forceinline__ int mark_point(double px, double py, int W, int H, Prev &prev,
+                                          Sink &sink)
+{
+    // the (up to) 2 x 2 candidate pixels, branch-free so lanes do not diverge
+    const Prev r = point_range(px, py);
+    int marks = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int ix = (k & 1) ? r.x1 : r.x0, iy = (k & 2) ? r.y1 : r.y0;
+        const bool dup = ((k & 1) && r.x1 == r.x0) || ((k & 2) && r.y1 == r.y0);
+        const bool seen = ix >= prev.x0 && ix <= prev.x1 && iy >= prev.y0 && iy <= prev.y1;
+        if (!dup && !seen && ix >= 0 && ix < W && iy >= 0 && iy < H) {
             sink(iy * (long long)W + ix);
+            marks++;
         }
     }
-    prev.x0 = ix0; prev.x1 = ix1; prev.y0 = iy0; prev.y1 = iy1;
+    prev = r;
+    return marks;
 }
 
 // One monotone list of grid-line crossing parameters along the clipped segment
-// (contrast.py:150-175): s_k = clamp01((k - c0) / dd) for integer k in
-// [ceil(min), floor(max)], enumerated in increasing-s order (k ascending when
-// dd > 0, descending when dd < 0).
-struct Crossings {
+// (contrast.py:150-175): item i is s = clamp01((k_i - c0) / dd) for the
+// integers k in [ceil(min), floor(max)], enumerated in increasing-s order
+// (k ascending when dd > 0, descending when dd < 0).
+struct CrossList {
     double c0, dd;
-    long long k, k_end;  // current and last k (inclusive)
-    int step;            // +1 / -1
-    bool live;
+    long long k0;
+    int n, step;
+
     __device__ __forceinline__ void init(double a0, double a1)
     {
         c0 = a0;
         dd = dsub(a1, a0);
-        if (dd == 0.0) { live = false; return; }
+        n = 0;
+        step = 1;
+        k0 = 0;
+        if (dd == 0.0) return;
         const double lo = a0 < a1 ? a0 : a1, hi = a0 < a1 ? a1 : a0;
         const long long kmin = (long long)ceil(lo), kmax = (long long)floor(hi);
-        if (kmin > kmax) { live = false; return; }
-        live = true;
-        if (dd > 0.0) { k = kmin; k_end = kmax; step = 1; }
-        else          { k = kmax; k_end = kmin; step = -1; }
+        if (kmin > kmax) return;
+        n = (int)(kmax - kmin + 1);
+        if (dd > 0.0) { k0 = kmin; step = 1; }
+        else          { k0 = kmax; step = -1; }
     }
-    __device__ __forceinline__ double value() const
+    __device__ __forceinline__ double at(int i) const
     {
-        double s = ddiv(dsub((double)k, c0), dd);
+        double s = ddiv(dsub((double)(k0 + (long long)step * i), c0), dd);
         if (s < 0.0) s = 0.0;
         else if (s > 1.0) s = 1.0;
         return s;
     }
-    __device__ __forceinline__ void advance()
+    // Index i of the first item >= v (items [0, i) are < v), found from an
+    // arithmetic estimate fixed up with exact item values; also returns the
+    // values of item i-1 (`below`, -1 if none) and item i (`above`, 2 if none).
+    __device__ int bound(double v, double &below, double &above) const
     {
-        if (k == k_end) live = false;
-        else k += step;
+        const double kv = dadd(c0, dmul(v, dd));
+        const double est = step > 0 ? ceil(kv - (double)k0) : ceil((double)k0 - kv);
+        int i = est < 0.0 ? 0 : (est > (double)n ? n : (int)est);
+        double lo = i > 0 ? at(i - 1) : -1.0;
+        double hi = i < n ? at(i) : 2.0;
+        while (i > 0 && lo >= v) {
+            i--;
+            hi = lo;
+            lo = i > 0 ? at(i - 1) : -1.0;
+        }
+        while (i < n && hi < v) {
+            i++;
+            lo = hi;
+            hi = i < n ? at(i) : 2.0;
+        }
+        below = lo;
+        above = hi;
+        return i;
     }
 };
 
-// _rasterize_into (contrast.py:94-182) for the closed segment a -> b, calling
-// sink(pixel) once for every in-image pixel whose closed square it touches.
-// Returns the number of sink calls.
+// A clipped segment ready for sampling.  Its sample sequence is
+// [0, merge(X, Y), 1] (np.sort of the reference's ts array: both lists are
+// monotone and clamped into [0, 1], so a two-way merge reproduces the sorted
+// multiset).  Long sequences are cut into `chunks` pieces by value: chunk j
+// holds the items with value in [j/J, (j+1)/J).  Crossings are uniformly
+// dense in the parameter, so the pieces hold nearly equal item counts, and
+// each piece finds its exact seams and its predecessor item with
+// CrossList::bound -- the marks equal one sequential pass.
+struct SegDesc {
+    CrossList X, Y;  // X.c0 = cx0, X.dd = ddx, Y.c0 = cy0, Y.dd = ddy
+    int chunks;
+};
+
+// Clip the closed segment a -> b (contrast.py:94-146).  Returns the number of
+// chunks to sample (0 if nothing is left to mark: off-frame, or degenerate /
+// single-pixel segments, which are marked here directly).
 template <class Sink>
-__device__ __noinline__ int raster_segment(double ax, double ay, double bx, double by,
-                                           int W, int H, Sink &sink)
+__device__ __forceinline__ int build_segment(double ax, double ay, double bx, double by, int W,
+                                             int H, int C, SegDesc &d, Sink &sink, int &marks)
 {
-    int marks = 0;
-    auto counted = [&](long long p) { marks++; sink(p); };
     if (ax == bx && ay == by) {  // degenerate: floor rule, not the closed-square rule
         const long long p = floor_bin(ax, ay, W, H);
-        if (p >= 0) counted(p);
-        return marks;
+        if (p >= 0) { sink(p); marks++; }
+        return 0;
     }
     // Division-free rejection, exact: every sample the reference would mark
     // lies within (|ax|+|bx|)*2^-50 of the x-extent [min(ax,bx), max(ax,bx)]
@@ -168,44 +211,183 @@ __device__ __noinline__ int raster_segment(double ax, double ay, double bx, doub
         }
         if (t0 > t1) return 0;
     }
-    const double cx0 = dadd(ax, dmul(t0, dx)), cy0 = dadd(ay, dmul(t0, dy));
-    const double cx1 = dadd(ax, dmul(t1, dx)), cy1 = dadd(ay, dmul(t1, dy));
-    Crossings X, Y;
-    X.init(cx0, cx1);
-    Y.init(cy0, cy1);
-    const double ddx = X.dd, ddy = Y.dd;
-    // np.sort(ts) == [0, merge(X, Y), 1]: both crossing lists are monotone and
-    // clamped into [0, 1], so a two-way merge reproduces the sorted multiset.
-    double sx = X.live ? X.value() : 2.0;
-    double sy = Y.live ? Y.value() : 2.0;
-    Prev prev{1, 0, 1, 0};
-    double cur = 0.0;
-    while (true) {
-        mark_point(dadd(cx0, dmul(cur, ddx)), dadd(cy0, dmul(cur, ddy)), W, H, prev, counted);
-        double nxt;
-        bool last = false;
-        if (X.live && (!Y.live || sx <= sy)) {
-            nxt = sx;
-            X.advance();
-            sx = X.live ? X.value() : 2.0;
-        } else if (Y.live) {
-            nxt = sy;
-            Y.advance();
-            sy = Y.live ? Y.value() : 2.0;
-        } else {
-            nxt = 1.0;
-            last = true;
-        }
-        const double sm = dmul(0.5, dadd(cur, nxt));
-        mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, prev, counted);
-        cur = nxt;
-        if (last) {
-            mark_point(dadd(cx0, dmul(cur, ddx)), dadd(cy0, dmul(cur, ddy)), W, H, prev, counted);
-            break;
+    // contrast.py:139-144
+    d.X.init(dadd(ax, dmul(t0, dx)), dadd(ax, dmul(t1, dx)));
+    d.Y.init(dadd(ay, dmul(t0, dy)), dadd(ay, dmul(t1, dy)));
+    if (d.X.n == 0 && d.Y.n == 0) {
+        // No crossings: the samples are ts = [0, 1] and the calls mark p(0),
+        // p(0.5), p(1).  If p(0) = (cx0, cy0) and p(1) = (cx0 + ddx, cy0 + ddy)
+        // lie strictly inside one pixel, so does p(0.5) (it lies between them
+        // coordinate-wise), and the three calls mark exactly that pixel.
+        const double x1 = dadd(d.X.c0, d.X.dd), y1 = dadd(d.Y.c0, d.Y.dd);
+        const double fx0 = floor(d.X.c0), fy0 = floor(d.Y.c0);
+        if (fx0 != d.X.c0 && fy0 != d.Y.c0 && floor(x1) == fx0 && floor(y1) == fy0 &&
+            x1 != fx0 && y1 != fy0) {
+            const long long p = floor_bin(d.X.c0, d.Y.c0, W, H);
+            if (p >= 0) { sink(p); marks++; }
+            return 0;
         }
     }
+    const int items = 2 + d.X.n + d.Y.n;
+    d.chunks = (items + C - 1) / C;
+    return d.chunks;
+}
+
+// Resumable walk over one chunk's items: mark every item, then the midpoint
+// to its successor (contrast.py:176-182).  Each list keeps its next two item
+// values, so the division that refills a list is off the critical path.
+struct Cursor {
+    int iX, iY, eX, eY;   // next unconsumed item of each list; chunk ends
+    double sX, sX2;       // values of X items iX, iX+1 (2 = none)
+    double sY, sY2;
+    double cur;           // item to mark next
+    double after;         // first item after the chunk (for its last midpoint)
+    Prev prev;
+    int last, fin;        // chunk ends with the trailing ts = 1; cur is that item
+};
+
+__device__ __forceinline__ double chunk_edge(int j, int J) { return (double)j / (double)J; }
+
+__device__ __forceinline__ double item_or_none(const CrossList &L, int i, int e)
+{
+    return i < e ? L.at(i) : 2.0;
+}
+
+// Position the cursor at chunk j of J; false if the chunk holds no item (its
+// neighbours then emit the midpoint across it).
+__device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
+{
+    const int J = d.chunks;
+    c.last = j == J - 1;
+    c.fin = 0;
+    c.prev = Prev{1, 0, 1, 0};
+    if (!c.last) {
+        double b, aX, aY;
+        const double vb = chunk_edge(j + 1, J);
+        c.eX = d.X.bound(vb, b, aX);
+        c.eY = d.Y.bound(vb, b, aY);
+        c.after = aX < aY ? aX : aY;
+        if (c.after >= 2.0) c.after = 1.0;  // no item >= vb: the trailing ts = 1 follows
+    } else {
+        c.eX = d.X.n;
+        c.eY = d.Y.n;
+        c.after = 2.0;
+    }
+    if (j == 0) {  // the leading ts = 0 starts the first chunk
+        c.iX = 0;
+        c.iY = 0;
+        c.cur = 0.0;
+        c.sX = item_or_none(d.X, 0, c.eX);
+        c.sY = item_or_none(d.Y, 0, c.eY);
+    } else {
+        double pX, fX, pY, fY;
+        const double va = chunk_edge(j, J);
+        c.iX = d.X.bound(va, pX, fX);
+        c.iY = d.Y.bound(va, pY, fY);
+        if (c.iX >= c.eX) fX = 2.0;
+        if (c.iY >= c.eY) fY = 2.0;
+        double first;
+        if (fX < 2.0 && fX <= fY) {
+            first = fX;
+            c.iX++;
+            fX = item_or_none(d.X, c.iX, c.eX);
+        } else if (fY < 2.0) {
+            first = fY;
+            c.iY++;
+            fY = item_or_none(d.Y, c.iY, c.eY);
+        } else if (c.last) {
+            first = 1.0;  // only the trailing ts = 1 remains
+            c.fin = 1;
+        } else {
+            return false;
+        }
+        // predecessor: the largest item < va, or the leading ts = 0
+        double p = pX > pY ? pX : pY;
+        if (p < 0.0) p = 0.0;
+        const double sm = dmul(0.5, dadd(p, first));
+        c.prev = point_range(dadd(d.X.c0, dmul(sm, d.X.dd)), dadd(d.Y.c0, dmul(sm, d.Y.dd)));
+        c.cur = first;
+        c.sX = fX;
+        c.sY = fY;
+    }
+    c.sX2 = item_or_none(d.X, c.iX + 1, c.eX);
+    c.sY2 = item_or_none(d.Y, c.iY + 1, c.eY);
+    return true;
+}
+
+// One item: mark it, advance to its successor (the list it comes from shifts
+// its lookahead and refills it with one division on selected operands, so
+// lanes stay converged), mark the midpoint.  Returns false once the chunk is
+// finished.
+template <class Sink>
+__device__ __forceinline__ bool cursor_step(const SegDesc &d, Cursor &c, int W, int H, Sink &sink,
+                                            int &marks)
+{
+    const double cx0 = d.X.c0, ddx = d.X.dd, cy0 = d.Y.c0, ddy = d.Y.dd;
+    marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H, c.prev,
+                        sink);
+    if (c.fin) return false;
+    const bool tX = c.sX < 2.0 && c.sX <= c.sY;
+    const bool tY = !tX && c.sY < 2.0;
+    double nxt;
+    if (tX || tY) {
+        nxt = tX ? c.sX : c.sY;
+        const int idx = (tX ? c.iX : c.iY) + 2;  // the item that enters the lookahead
+        const int lim = tX ? c.eX : c.eY;
+        const long long k = tX ? d.X.k0 + (long long)d.X.step * idx
+                               : d.Y.k0 + (long long)d.Y.step * idx;
+        double v = ddiv(dsub((double)k, tX ? cx0 : cy0), tX ? ddx : ddy);
+        v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        if (idx >= lim) v = 2.0;
+        if (tX) {
+            c.iX++;
+            c.sX = c.sX2;
+            c.sX2 = v;
+        } else {
+            c.iY++;
+            c.sY = c.sY2;
+            c.sY2 = v;
+        }
+    } else if (c.last) {
+        nxt = 1.0;  // the trailing ts = 1
+        c.fin = 1;
+    } else {
+        const double sm = dmul(0.5, dadd(c.cur, c.after));  // midpoint into the next chunk
+        marks += mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev,
+                            sink);
+        return false;
+    }
+    const double sm = dmul(0.5, dadd(c.cur, nxt));
+    marks += mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
+    c.cur = nxt;
+    return true;
+}
+
+// Sample chunk j of a built segment to the end.
+template <class Sink>
+__device__ __forceinline__ int sample_chunk(const SegDesc &d, int j, int W, int H, Sink &sink)
+{
+    Cursor c;
+    int marks = 0;
+    if (cursor_init(d, j, c))
+        while (cursor_step(d, c, W, H, sink, marks)) {
+        }
     return marks;
 }
+
+// _rasterize_into (contrast.py:94-182) for one segment by one thread, chunk
+// by chunk (chunk size C only moves the seams).  Returns the sink calls.
+template <class Sink>
+__device__ int raster_segment(double ax, double ay, double bx, double by, int W, int H, int C,
+                              Sink &sink)
+{
+    SegDesc d;
+    int marks = 0;
+    const int chunks = build_segment(ax, ay, bx, by, W, H, C, d, sink, marks);
+    for (int j = 0; j < chunks; j++) marks += sample_chunk(d, j, W, H, sink);
+    return marks;
+}
+
 
 // ---------------------------------------------------------------- reductions
 template <class T>
@@ -248,31 +430,51 @@ __device__ __forceinline__ void block_add_u64(unsigned long long (&v)[K],
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is three xor-shuffle steps (IEEE
 // addition is commutative, only association matters), and lane 0 adds the
 // n % 8 tail sequentially.  n < 8 (only when M < 8) is the sequential branch.
-// q(i) yields the i-th summand.  Result valid in lane (j == 0) of the group.
+// All loads of the leaf are issued before the first add (one memory round
+// trip).  Q provides load(i) -> raw, term(raw) -> summand, clear(i).
 template <class Q>
 __device__ __forceinline__ double pairwise_leaf8(int off, int n, int j, const Q &q)
 {
     const unsigned gmask = 0xffu << (threadIdx.x & 24);
     if (n < 8) {
         double r = 0.0;
-        if (j == 0)
-            for (int i = 0; i < n; i++) r = dadd(r, q(off + i));
+        if (j == 0) {
+            for (int i = 0; i < n; i++) r = dadd(r, q.term(q.load(off + i)));
+            for (int i = 0; i < n; i++) q.clear(off + i);
+        }
         return r;
     }
-    double r = q(off + j);
-    const int body = n - (n % 8);
-    for (int i = 8; i < body; i += 8) r = dadd(r, q(off + i + j));
+    const int body = n - (n % 8), rows = body / 8;  // rows in [1, 16]
+    typename Q::raw v[16], tail[7];
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+        if (k < rows) v[k] = q.load(off + 8 * k + j);
+#pragma unroll
+    for (int k = 0; k < 7; k++)
+        if (j == 0 && body + k < n) tail[k] = q.load(off + body + k);
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+        if (k < rows) q.clear(off + 8 * k + j);
+    if (j == 0)
+        for (int k = body; k < n; k++) q.clear(off + k);
+    double r = q.term(v[0]);
+#pragma unroll
+    for (int k = 1; k < 16; k++)
+        if (k < rows) r = dadd(r, q.term(v[k]));
     r = dadd(r, __shfl_xor_sync(gmask, r, 1, 8));
     r = dadd(r, __shfl_xor_sync(gmask, r, 2, 8));
     r = dadd(r, __shfl_xor_sync(gmask, r, 4, 8));
-    if (j == 0)
-        for (int i = body; i < n; i++) r = dadd(r, q(off + i));
+    if (j == 0) {
+#pragma unroll
+        for (int k = 0; k < 7; k++)
+            if (body + k < n) r = dadd(r, q.term(tail[k]));
+    }
     return r;
 }
 
 // ---------------------------------------------------------------- grid barrier
-// Sense-counting barrier for a cooperative (co-resident) grid; the last block
-// to arrive optionally runs `leader` before releasing the others.
+// Counting barrier for a cooperative (co-resident) grid; the last block to
+// arrive optionally runs `leader` before releasing the others.
 struct GridBar {
     unsigned int count;
     unsigned int gen;

@@ -26,7 +26,7 @@ struct TreeDev {
     double *cutval;          // [C] scratch
 };
 
-struct FrontierEntry {
+struct alignas(32) FrontierEntry {
     double bound;
     long long counter;
     double lo, hi;
@@ -40,9 +40,9 @@ struct SolveState {
     // node under evaluation
     double lo, hi, c, den_lo, den_c, den_hi;
     int mode, done;
-    // per-iteration accumulators: 0 in_image, 1 fully_inside A, 2 fully_inside B,
-    // 3 S_bar A, 4 S_bar B, 5 marks A, 6 marks B
-    unsigned long long acc[8];
+    // per-node accumulators, double-buffered by node parity: 0 in_image,
+    // 1 fully_inside A, 2 fully_inside B, 3 S_bar A, 4 S_bar B
+    unsigned long long acc[2][8];
     // incumbent and diagnostics
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
@@ -63,6 +63,27 @@ struct SolveArgs {
     FrontierEntry *fr;
     long long fr_cap;
     void *bar;                // GridBar
+    long long *trace;         // [1 + kTraceSlots*trace_iters] globaltimer ns
+    long long trace_iters;
+    long long *btrace;        // [kBTraceIters][gridDim][4] per-block timestamps (or null)
+};
+
+constexpr int kBTraceIters = 128;
+constexpr int kBTraceSlots = 16;
+constexpr int kBTraceMaxBlocks = 2048;
+
+constexpr long long kTraceIters = 1 << 14;
+constexpr int kTraceSlots = 8;
+// per node evaluation: when ...
+enum TraceSlot : int {
+    kTrB0Top = 0,      // block 0 starts the node
+    kTrB0Events = 1,   // block 0 finished its events
+    kTrEventsMax = 2,  // the latest block finished its events (atomicMax)
+    kTrB0Pixels0 = 3,  // block 0 left barrier 1
+    kTrB0Pixels1 = 4,  // block 0 finished its pixels
+    kTrPixelsMax = 5,  // the latest block finished its pixels (atomicMax)
+    kTrB0Step0 = 6,    // block 0 left barrier 2
+    kTrB0Step1 = 7,    // block 0 finished the BnB step
 };
 
 // ---- kernel launchers (evd_kernels.cu); all asynchronous on `s` ----
@@ -84,7 +105,7 @@ void launch_contrast_u32(const unsigned int *img, const unsigned long long *in_i
                          const TreeDev &tree, double *out, cudaStream_t s);
 void launch_contrast_f64(const double *img, double mu, const TreeDev &tree, double *out,
                          cudaStream_t s);
-void launch_raster_segments(const double *segs, int k, int W, int H, unsigned int *counts,
+void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, unsigned int *counts,
                             cudaStream_t s);
 int solve_grid_blocks(int device);
 int solve_block_threads();

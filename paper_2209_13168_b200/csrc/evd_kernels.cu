@@ -2,7 +2,7 @@
 //
 // Standalone kernels back the per-call entry points (accumulate_image,
 // upper_bound_image, bound_terms, image_contrast, rasterize_segment,
-// radial_warp); k_solve is the device-resident branch-and-bound
+// radial_warp); k_solve is the device-resident branch and bound
 // (solver.py:79-123) that evaluates one node per grid-wide step.
 #include <cfloat>
 #include <climits>
@@ -13,7 +13,13 @@
 namespace evd {
 
 constexpr int kThreads = 256;
-constexpr int kSolveThreads = 512;
+#ifndef EVD_SOLVE_THREADS
+#define EVD_SOLVE_THREADS 512
+#define EVD_SOLVE_MINB 1
+#endif
+constexpr int kSolveThreads = EVD_SOLVE_THREADS;
+constexpr int kChunk = 32;            // sample items per supercover chunk
+constexpr int kInlineCrossings = 6;   // shorter segments are sampled by their own lane
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -39,6 +45,74 @@ struct AtomicSink {
     unsigned int *img;
     __device__ __forceinline__ void operator()(long long p) const { atomicAdd(img + p, 1u); }
 };
+
+// Per-warp queue of built segments: lane l owns slots 2l, 2l+1.
+struct WarpQueue {
+    SegDesc d[64];
+    int off[33];  // exclusive prefix of chunk counts per lane
+    int na[32];   // chunks of the lane's first segment
+};
+
+// Build one segment; sample it in the lane when it has at most one crossing,
+// otherwise queue it in the lane's shared-memory slot for warp_drain.
+// Returns the number of queued chunks.
+template <class Sink>
+__device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
+                                                int H, SegDesc &slot, Sink &sink, int &marks)
+{
+    SegDesc d;
+    const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
+    if (c == 0) return 0;
+    if (d.X.n + d.Y.n <= kInlineCrossings) {
+        marks += sample_chunk(d, 0, W, H, sink);
+        return 0;
+    }
+    slot = d;
+    return c;
+}
+
+// Sample every chunk the warp queued, in rounds of 32: all lanes position
+// their cursors together, then step one item per iteration; chunks hold
+// nearly equal item counts, so the lanes stay converged.
+__device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H,
+                                          unsigned int *imgA, unsigned int *imgB)
+{
+    const int lane = threadIdx.x & 31;
+    int incl = cA + cB;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    q.off[lane + 1] = incl;
+    if (lane == 0) q.off[0] = 0;
+    q.na[lane] = cA;
+    __syncwarp();
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int marks = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int t = base + lane;
+        bool active = false;
+        int slot = 0;
+        Cursor c;
+        AtomicSink sink{imgA};
+        if (t < total) {
+            int L = 0;  // largest lane with off[L] <= t
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1)
+                if (q.off[L + s] <= t) L += s;
+            const int r = t - q.off[L];
+            const bool second = r >= q.na[L];
+            slot = 2 * L + (second ? 1 : 0);
+            if (second) sink.img = imgB;
+            active = cursor_init(q.d[slot], second ? r - q.na[L] : r, c);
+        }
+        while (__any_sync(0xffffffffu, active))
+            if (active) active = cursor_step(q.d[slot], c, W, H, sink, marks);
+    }
+    __syncwarp();
+    return marks;
+}
 
 // ---------------------------------------------------------------- elementwise
 __global__ void k_center(const double *__restrict__ x, const double *__restrict__ y, long long n,
@@ -91,22 +165,32 @@ __global__ void k_point_image(const double *__restrict__ xc, const double *__res
     block_add_u64<1>(v, acc);
 }
 
-// _bound_image_kernel (contrast.py:185-203) on warps at lo/hi:
-// acc[0] += fully-inside segments, acc[1] += marks (= sum of the image)
-__global__ void k_bound_image(const double *__restrict__ xc, const double *__restrict__ yc,
-                              const double *__restrict__ t, long long n, double lo, double den_lo,
-                              double hi, double den_hi, double cx, double cy, int W, int H,
-                              unsigned int *img, unsigned long long *acc)
+// _bound_image_kernel (contrast.py:185-203) on warps at lo/hi, long segments
+// spread over the warp: acc[0] += fully-inside segments, acc[1] += marks
+__global__ void __launch_bounds__(kThreads) k_bound_image(
+    const double *__restrict__ xc, const double *__restrict__ yc, const double *__restrict__ t,
+    long long n, double lo, double den_lo, double hi, double den_hi, double cx, double cy, int W,
+    int H, unsigned int *img, unsigned long long *acc)
 {
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
     unsigned long long v[2] = {0, 0};
     AtomicSink sink{img};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const double x = __ldg(xc + i), y = __ldg(yc + i), tt = __ldg(t + i);
-        const Warped a = warp_event(x, y, tt, lo, den_lo, cx, cy);
-        const Warped b = warp_event(x, y, tt, hi, den_hi, cx, cy);
-        v[0] += fully_inside(a.x, a.y, b.x, b.y, W, H);
-        v[1] += raster_segment(a.x, a.y, b.x, b.y, W, H, sink);
+    const long long gsz = (long long)gridDim.x * blockDim.x;
+    for (long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); base < n;
+         base += gsz) {
+        const long long i = base + lane;
+        int c = 0, marks = 0;
+        if (i < n) {
+            const double x = __ldg(xc + i), y = __ldg(yc + i), tt = __ldg(t + i);
+            const Warped a = warp_event(x, y, tt, lo, den_lo, cx, cy);
+            const Warped b = warp_event(x, y, tt, hi, den_hi, cx, cy);
+            v[0] += fully_inside(a.x, a.y, b.x, b.y, W, H);
+            c = segment_or_queue(a.x, a.y, b.x, b.y, W, H, wq.d[2 * lane], sink, marks);
+        }
+        if (__any_sync(0xffffffffu, c != 0)) marks += warp_drain(wq, c, 0, W, H, img, img);
+        v[1] += marks;
     }
     block_add_u64<2>(v, acc);
 }
@@ -125,45 +209,46 @@ __global__ void k_image_sums(const unsigned int *__restrict__ img, long long m,
     block_add_u64<2>(v, acc);
 }
 
-// rasterize_segment (contrast.py:206-222) for k segments, one thread each:
-// counts[j*M + p] is incremented once per mark (a dedup failure shows as 2).
+// rasterize_segment (contrast.py:206-222) for k segments, one thread each
+// (all chunks of size `chunk` in order): counts[j*M + p] is incremented once
+// per mark, so a dedup failure would show as 2.
 __global__ void k_raster_segments(const double *__restrict__ segs, int k, int W, int H,
-                                  unsigned int *counts)
+                                  int chunk, unsigned int *counts)
 {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= k) return;
     unsigned int *img = counts + (long long)j * W * H;
     auto sink = [img](long long p) { img[p] += 1u; };
-    raster_segment(segs[4 * j], segs[4 * j + 1], segs[4 * j + 2], segs[4 * j + 3], W, H, sink);
+    raster_segment(segs[4 * j], segs[4 * j + 1], segs[4 * j + 2], segs[4 * j + 3], W, H, chunk,
+                   sink);
 }
 
 // ---------------------------------------------------------------- contrast tree
-// Summands of image_contrast (contrast.py:64): (H_p - mu)**2, numpy square.
+// Summands of image_contrast (contrast.py:64): (H_p - mu)**2 (numpy square).
 struct SqU32 {
+    typedef unsigned int raw;
     const unsigned int *img;
     double mu;
-    __device__ __forceinline__ double operator()(int i) const
+    __device__ __forceinline__ raw load(int i) const { return __ldcg(img + i); }
+    __device__ __forceinline__ void clear(int) const {}
+    __device__ __forceinline__ double term(raw h) const
     {
-        const double d = dsub((double)__ldcg(img + i), mu);
+        const double d = dsub((double)h, mu);
         return dmul(d, d);
     }
 };
-struct SqU32Clear {  // same, and leaves the pixel zeroed for the next BnB node
-    unsigned int *img;
-    double mu;
-    __device__ __forceinline__ double operator()(int i) const
-    {
-        const double d = dsub((double)__ldcg(img + i), mu);
-        img[i] = 0u;
-        return dmul(d, d);
-    }
+struct SqU32Clear : SqU32 {  // and leave the pixel zeroed for the next BnB node
+    __device__ __forceinline__ void clear(int i) const { const_cast<unsigned int *>(img)[i] = 0u; }
 };
 struct SqF64 {
+    typedef double raw;
     const double *img;
     double mu;
-    __device__ __forceinline__ double operator()(int i) const
+    __device__ __forceinline__ raw load(int i) const { return __ldcg(img + i); }
+    __device__ __forceinline__ void clear(int) const {}
+    __device__ __forceinline__ double term(raw c) const
     {
-        const double d = dsub(__ldcg(img + i), mu);
+        const double d = dsub(c, mu);
         return dmul(d, d);
     }
 };
@@ -238,51 +323,184 @@ __global__ void k_contrast_top(TreeDev T, double *out)
 }
 
 // ---------------------------------------------------------------- BnB solve
+// The solve is a replicated state machine: every block holds the same BnB
+// control state (Replica, shared memory) and, after the grid barrier that
+// completes a node's pixel reductions, every block computes the identical
+// (deterministic) next step itself -- no serial leader, no release round.
+// Global memory carries only what must be shared: images, per-node integer
+// accumulators (double-buffered by parity), the cut sums of the contrast tree,
+// and the frontier, whose writes block 0 commits one phase later (after the
+// next barrier) so no block can still be reading the entries it replaces.
+
+__device__ __forceinline__ long long globaltimer()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Solve trace (globaltimer ns): trace[0] = kernel start, then kTraceSlots per
+// node evaluation i (0 = root) at 1 + kTraceSlots*i + slot, see TraceSlot.
+__device__ __forceinline__ void trace_point(const SolveArgs &a, long long it, int slot)
+{
+    if (!a.trace || threadIdx.x != 0) return;
+    if (slot < 0) a.trace[0] = globaltimer();
+    else if (it < a.trace_iters) a.trace[1 + kTraceSlots * it + slot] = globaltimer();
+}
+__device__ __forceinline__ void trace_max(const SolveArgs &a, long long it, int slot)
+{
+    if (!a.trace || threadIdx.x != 0 || it >= a.trace_iters) return;
+    atomicMax(reinterpret_cast<unsigned long long *>(a.trace + 1 + kTraceSlots * it + slot),
+              (unsigned long long)globaltimer());
+}
+
+__device__ __forceinline__ void btrace_point(const SolveArgs &a, long long it, int k)
+{
+    if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
+    a.btrace[(it * gridDim.x + blockIdx.x) * kBTraceSlots + k] = globaltimer();
+}
+// sub-phase markers (SM cycles) in slots 4.. of the block trace
+__device__ __forceinline__ void bclock(const SolveArgs &a, long long it, int k)
+{
+    if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
+    a.btrace[(it * gridDim.x + blockIdx.x) * kBTraceSlots + k] = clock64();
+}
+
+// Grid barrier on a monotone 64-bit arrival counter (no reset round trip):
+// the n-th barrier completes when the counter reaches n * gridDim.x.
+__device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long long &target)
+{
+    target += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ bool better(double b1, long long c1, double b2, long long c2)
 {
     // heapq order on (-c_bar, counter): larger bound first, FIFO among ties
     return b1 > b2 || (b1 == b2 && c1 < c2);
 }
 
-__device__ void frontier_push(const SolveArgs &a, volatile SolveState *st, double bound,
-                              double lo, double hi)
+// 32-byte frontier entries moved as two 16-byte L2 (.cg) accesses
+__device__ __forceinline__ void entry_store(FrontierEntry *dst, const FrontierEntry &e)
 {
-    const long long n = st->fr_n;
-    if (n >= a.fr_cap) {
-        st->status = kStatusCapacity;
-        st->done = 1;
-        return;
-    }
-    volatile FrontierEntry *e = a.fr + n;
-    e->bound = bound;
-    e->counter = st->next_counter;
-    e->lo = lo;
-    e->hi = hi;
-    st->next_counter = st->next_counter + 1;
-    st->fr_n = n + 1;
-    if (n + 1 > st->max_fr) st->max_fr = n + 1;
+    const double2 *src = reinterpret_cast<const double2 *>(&e);
+    __stcg(reinterpret_cast<double2 *>(dst), src[0]);
+    __stcg(reinterpret_cast<double2 *>(dst) + 1, src[1]);
+}
+__device__ __forceinline__ FrontierEntry entry_load(const FrontierEntry *src)
+{
+    FrontierEntry e;
+    double2 *d = reinterpret_cast<double2 *>(&e);
+    d[0] = __ldcg(reinterpret_cast<const double2 *>(src));
+    d[1] = __ldcg(reinterpret_cast<const double2 *>(src) + 1);
+    return e;
 }
 
-// Pop the best frontier node and run the termination test (solver.py:102-108);
-// otherwise make it the next node to evaluate.  Whole block.
-__device__ void frontier_pop(const SolveArgs &a)
+// BnB control state, identical in every block.
+struct Replica {
+    double lo, hi, c, den_lo, den_c, den_hi;  // node under evaluation
+    int mode, done, status, parity;
+    double nu_hat, c_hat, bound_gap;
+    long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
+    // this node's integer accumulators and pow(fi/M, 2) table values
+    unsigned long long fiA, fiB, sA, sB;
+    double p2A, p2B;
+    // frontier writes of the last step, committed by block 0 after the next barrier
+    int n_pending;
+    long long pend_idx[3];
+    FrontierEntry pend[3];
+    // entries pushed by the current step (indices fr_n_before + k)
+    int n_pushed;
+    FrontierEntry pushed[2];
+};
+
+constexpr int kFrView = 1024;  // frontier entries staged in shared memory per step
+
+__device__ __forceinline__ void replica_push(const SolveArgs &a, Replica &R, long long n0,
+                                             double bound, double lo, double hi)
 {
-    volatile SolveState *st = a.st;
-    __shared__ long long s_n;
-    __shared__ double r_b[32];
-    __shared__ long long r_c[32], r_i[32];
-    if (threadIdx.x == 0) s_n = st->fr_n;
-    __syncthreads();
-    const long long n = s_n;
-    if (n == 0) {  // queue exhausted: every interval pruned, gap closed (solver.py:121-122)
-        if (threadIdx.x == 0) st->done = 1;
+    if (n0 + R.n_pushed >= a.fr_cap) {
+        R.status = kStatusCapacity;
+        R.done = 1;
         return;
     }
+    const FrontierEntry e{bound, R.next_counter++, lo, hi};
+    R.pushed[R.n_pushed] = e;
+    R.pend_idx[R.n_pending] = n0 + R.n_pushed;
+    R.pend[R.n_pending] = e;
+    R.n_pending++;
+    R.n_pushed++;
+}
+
+// One BnB step (solver.py:102-119 from the centre evaluation on): incumbent
+// update with >=, both child bounds assembled as contrast.py:248-251, pruning
+// with >=, the iteration cap, then the best-first pop and stop test of the
+// next iteration.  Whole block; identical in every block.  Frontier entries
+// [0, fr_n) are in `view` when fr_n <= kFrView (else read from global).
+__device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const FrontierEntry *view)
+{
+    const long long n0 = R.fr_n;
+    const bool staged = n0 <= kFrView;
+    if (threadIdx.x == 0) {
+        const double M = (double)a.tree.M;
+        const double C = ddiv(dadd(0.0, S), M);  // np.sum(...) / M
+        R.n_pending = 0;
+        R.n_pushed = 0;
+        R.point_evals++;
+        if (R.mode == kModeRoot) {
+            R.c_hat = C;
+            R.nu_hat = R.c;
+            const double cb = dsub(ddiv((double)R.sA, M), R.p2A);
+            R.bound_evals++;
+            replica_push(a, R, n0, cb, R.lo, R.hi);
+        } else {
+            if (C >= R.c_hat) {  // solver.py:111
+                R.nu_hat = R.c;
+                R.c_hat = C;
+            }
+            const double cbA = dsub(ddiv((double)R.sA, M), R.p2A);
+            const double cbB = dsub(ddiv((double)R.sB, M), R.p2B);
+            R.bound_evals += 2;
+            if (cbA >= R.c_hat) replica_push(a, R, n0, cbA, R.lo, R.c);
+            if (cbB >= R.c_hat && !R.done) replica_push(a, R, n0, cbB, R.c, R.hi);
+            if (R.iterations >= a.max_iter && !R.done) {
+                R.status = kStatusIterLimit;
+                R.done = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (R.done) return;
+    const long long n1 = n0 + R.n_pushed;
+    if (n1 == 0) {  // queue exhausted: every interval pruned (solver.py:121-122)
+        __syncthreads();
+        if (threadIdx.x == 0) R.done = 1;
+        __syncthreads();
+        return;
+    }
+    auto entry = [&](long long i) -> FrontierEntry {
+        if (i >= n0) return R.pushed[i - n0];
+        return staged ? view[i] : entry_load(a.fr + i);
+    };
+    // best-first pop: argmax over the committed entries and this step's pushes
+    __shared__ double r_b[32];
+    __shared__ long long r_c[32], r_i[32];
     double bb = -DBL_MAX;
     long long bc = LLONG_MAX, bi = -1;
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        const double b = __ldcg(&a.fr[i].bound);
-        const long long c = __ldcg(&a.fr[i].counter);
+    for (long long i = threadIdx.x; i < n1; i += blockDim.x) {
+        double b;
+        long long c;
+        if (i >= n0) { b = R.pushed[i - n0].bound; c = R.pushed[i - n0].counter; }
+        else if (staged) { b = view[i].bound; c = view[i].counter; }
+        else { b = __ldcg(&a.fr[i].bound); c = __ldcg(&a.fr[i].counter); }
         if (bi < 0 || better(b, c, bb, bc)) { bb = b; bc = c; bi = i; }
     }
 #pragma unroll
@@ -300,136 +518,296 @@ __device__ void frontier_pop(const SolveArgs &a)
             if (r_i[w] >= 0 && (bi < 0 || better(r_b[w], r_c[w], bb, bc))) {
                 bb = r_b[w]; bc = r_c[w]; bi = r_i[w];
             }
-        volatile FrontierEntry *e = a.fr + bi;
-        const double lo = e->lo, hi = e->hi;
-        volatile FrontierEntry *last = a.fr + (n - 1);
-        e->bound = last->bound;
-        e->counter = last->counter;
-        e->lo = last->lo;
-        e->hi = last->hi;
-        st->fr_n = n - 1;
-        st->iterations = st->iterations + 1;
-        const double gap = dsub(bb, st->c_hat);  // -(-c_bar) - c_hat
-        if (gap <= a.gamma || dsub(hi, lo) < a.min_width) {
-            st->bound_gap = (0.0 > gap) ? 0.0 : gap;  // Python max(gap, 0.0)
-            st->done = 1;
-        } else {
-            const double c = dmul(0.5, dadd(lo, hi));  // VelocityInterval.center
-            st->lo = lo;
-            st->hi = hi;
-            st->c = c;
-            st->den_lo = dadd(1.0, dmul(lo, a.tau));
-            st->den_c = dadd(1.0, dmul(c, a.tau));
-            st->den_hi = dadd(1.0, dmul(hi, a.tau));
-            st->mode = kModeNode;
+        const FrontierEntry top = entry(bi);
+        const long long last = n1 - 1;
+        if (bi != last) {  // swap-remove: the last entry takes the popped slot
+            R.pend_idx[R.n_pending] = bi;
+            R.pend[R.n_pending] = entry(last);
+            R.n_pending++;
         }
-    }
-}
-
-// Runs in the last block to arrive at the end of an iteration: finish the
-// contrast of the centre, assemble the child bounds (contrast.py:248-251),
-// incumbent update / pruning (solver.py:110-119), then pop the next node.
-__device__ void leader_step(const SolveArgs &a, double *scratch)
-{
-    volatile SolveState *st = a.st;
-    const double S = eval_top(a.tree, scratch);
-    __shared__ int s_done;
-    if (threadIdx.x == 0) {
-        const double M = (double)a.tree.M;
-        const double C = ddiv(dadd(0.0, S), M);
-        const double lo = st->lo, hi = st->hi, c = st->c;
-        const unsigned long long fiA = st->acc[1], fiB = st->acc[2];
-        const unsigned long long sA = st->acc[3], sB = st->acc[4];
-        st->point_evals = st->point_evals + 1;
-        if (st->mode == kModeRoot) {
-            st->c_hat = C;
-            st->nu_hat = c;
-            const double cb = dsub(ddiv((double)sA, M), a.pow2[fiA]);
-            st->bound_evals = st->bound_evals + 1;
-            frontier_push(a, st, cb, lo, hi);
+        R.fr_n = n1 - 1;
+        if (n1 > R.max_fr) R.max_fr = n1;
+        R.iterations++;
+        const double gap = dsub(bb, R.c_hat);  // -(-c_bar) - c_hat
+        if (gap <= a.gamma || dsub(top.hi, top.lo) < a.min_width) {
+            R.bound_gap = (0.0 > gap) ? 0.0 : gap;  // Python max(gap, 0.0)
+            R.done = 1;
         } else {
-            if (C >= st->c_hat) {  // solver.py:111 uses >=
-                st->nu_hat = c;
-                st->c_hat = C;
-            }
-            const double cbA = dsub(ddiv((double)sA, M), a.pow2[fiA]);
-            const double cbB = dsub(ddiv((double)sB, M), a.pow2[fiB]);
-            st->bound_evals = st->bound_evals + 2;
-            if (cbA >= st->c_hat) frontier_push(a, st, cbA, lo, c);
-            if (cbB >= st->c_hat) frontier_push(a, st, cbB, c, hi);
-            if (st->iterations >= a.max_iter && !st->done) {
-                st->status = kStatusIterLimit;
-                st->done = 1;
-            }
+            const double c = dmul(0.5, dadd(top.lo, top.hi));  // VelocityInterval.center
+            R.lo = top.lo;
+            R.hi = top.hi;
+            R.c = c;
+            R.den_lo = dadd(1.0, dmul(top.lo, a.tau));
+            R.den_c = dadd(1.0, dmul(c, a.tau));
+            R.den_hi = dadd(1.0, dmul(top.hi, a.tau));
+            R.mode = kModeNode;
         }
-        for (int k = 0; k < 8; k++) st->acc[k] = 0ull;
-        s_done = st->done;
     }
     __syncthreads();
-    if (!s_done) frontier_pop(a);
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 1) k_solve(SolveArgs a)
+// Per-block shared-memory copy of the reduction-tree metadata this block
+// touches (its own cuts, and the top): after every barrier the L1 is
+// invalidated, so tables left in global memory would cost a dependent L2
+// round trip per tree level.
+constexpr int kCacheCuts = 8, kCacheLeaves = 1024, kCacheTrips = 1024, kCacheTop = 1024;
+struct TreeCache {
+    int2 leaves[kCacheLeaves];
+    int4 trip[kCacheTrips];
+    int4 top[kCacheTop];
+    int cut_leaf0[kCacheCuts + 1], cut_trip0[kCacheCuts + 1], cut_nlev[kCacheCuts];
+    int cut_lvl[kCacheCuts * (kMaxLevels + 1)];
+    int top_lvl[kMaxLevels + 1];
+};
+
+// Returns a TreeDev whose cut index q means global cut blockIdx.x + q*gridDim.x
+// (local = true), or the global tables when they do not fit (local = false).
+__device__ TreeDev cache_tree(const TreeDev &g, TreeCache &tc, bool &local)
 {
-    __shared__ double scratch[kCutSmem];
-    GridBar *bar = (GridBar *)a.bar;
-    volatile SolveState *st = a.st;
+    __shared__ int s_ok, s_nq;
+    if (threadIdx.x == 0) {
+        int nq = g.C > (int)blockIdx.x ? (g.C - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        int ok = nq <= kCacheCuts && g.top_lvl[g.top_levels] <= kCacheTop &&
+                 g.top_levels <= kMaxLevels;
+        int nl = 0, nt = 0;
+        for (int q = 0; ok && q < nq; q++) {
+            const int c = blockIdx.x + q * gridDim.x;
+            tc.cut_leaf0[q] = nl;
+            tc.cut_trip0[q] = nt;
+            nl += g.cut_leaf0[c + 1] - g.cut_leaf0[c];
+            nt += g.cut_trip0[c + 1] - g.cut_trip0[c];
+            tc.cut_nlev[q] = g.cut_nlev[c];
+        }
+        ok = ok && nl <= kCacheLeaves && nt <= kCacheTrips;
+        tc.cut_leaf0[nq] = nl;
+        tc.cut_trip0[nq] = nt;
+        s_ok = ok;
+        s_nq = nq;
+    }
+    __syncthreads();
+    local = s_ok != 0;
+    if (!local) return g;  // does not fit: read the global tables
+    const int nq = s_nq;
+    for (int q = 0; q < nq; q++) {
+        const int c = blockIdx.x + q * gridDim.x;
+        const int l0 = g.cut_leaf0[c], nl = g.cut_leaf0[c + 1] - l0;
+        const int t0 = g.cut_trip0[c], nt = g.cut_trip0[c + 1] - t0;
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) tc.leaves[tc.cut_leaf0[q] + i] = g.leaves[l0 + i];
+        for (int i = threadIdx.x; i < nt; i += blockDim.x) tc.trip[tc.cut_trip0[q] + i] = g.trip[t0 + i];
+        for (int i = threadIdx.x; i <= kMaxLevels; i += blockDim.x)
+            tc.cut_lvl[q * (kMaxLevels + 1) + i] = g.cut_lvl[(long long)c * (kMaxLevels + 1) + i];
+    }
+    const int ntop = g.top_lvl[g.top_levels];
+    for (int i = threadIdx.x; i < ntop; i += blockDim.x) tc.top[i] = g.top[i];
+    for (int i = threadIdx.x; i <= g.top_levels; i += blockDim.x) tc.top_lvl[i] = g.top_lvl[i];
+    __syncthreads();
+    TreeDev t = g;
+    t.leaves = tc.leaves;
+    t.cut_leaf0 = tc.cut_leaf0;
+    t.cut_trip0 = tc.cut_trip0;
+    t.cut_lvl = tc.cut_lvl;
+    t.cut_nlev = tc.cut_nlev;
+    t.trip = tc.trip;
+    t.top = tc.top;
+    t.top_lvl = tc.top_lvl;
+    return t;
+}
+
+// Combine the C cut sums (already staged in v) through the top of the tree.
+__device__ double top_combine(const TreeDev &T, double *v)
+{
+    for (int h = 0; h < T.top_levels; h++) {
+        for (int k = T.top_lvl[h] + threadIdx.x; k < T.top_lvl[h + 1]; k += blockDim.x) {
+            const int4 tr = T.top[k];
+            v[tr.x] = dadd(v[tr.y], v[tr.z]);
+        }
+        __syncthreads();
+    }
+    const double r = v[T.top_root];
+    __syncthreads();
+    return r;
+}
+
+constexpr size_t kQueueBytes = sizeof(WarpQueue) * (kSolveThreads / 32);
+constexpr size_t kStepBytes = kCutSmem * sizeof(double) + kFrView * sizeof(FrontierEntry);
+constexpr size_t kRegionA = kQueueBytes > kStepBytes ? kQueueBytes : kStepBytes;
+constexpr size_t kSolveSmemBytes = kRegionA + sizeof(TreeCache);
+
+__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    // region A: warp queues (event phase) | cut scratch + frontier view (pixels, step)
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    double *scratch = reinterpret_cast<double *>(smem);
+    FrontierEntry *view = reinterpret_cast<FrontierEntry *>(smem + kCutSmem * sizeof(double));
+    TreeCache &tc = *reinterpret_cast<TreeCache *>(smem + kRegionA);
+    __shared__ Replica R;
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(a.bar);
+    unsigned long long target = 0;
+    SolveState *st = a.st;
+    const int lane = threadIdx.x & 31;
     const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long gsz = (long long)gridDim.x * blockDim.x;
     const int W = a.W, H = a.H;
-    while (true) {
-        if (st->done) break;
-        const int mode = st->mode;
-        const double lo = st->lo, hi = st->hi, c = st->c;
-        const double den_lo = st->den_lo, den_c = st->den_c, den_hi = st->den_hi;
-        __syncthreads();
+    bool local_cuts;
+    const TreeDev tree = cache_tree(a.tree, tc, local_cuts);
+    if (threadIdx.x == 0) {
+        R.lo = __ldcg(&st->lo);
+        R.hi = __ldcg(&st->hi);
+        R.c = __ldcg(&st->c);
+        R.den_lo = __ldcg(&st->den_lo);
+        R.den_c = __ldcg(&st->den_c);
+        R.den_hi = __ldcg(&st->den_hi);
+        R.mode = kModeRoot;
+        R.done = 0;
+        R.status = kStatusOk;
+        R.parity = 0;
+        R.nu_hat = 0.0;
+        R.c_hat = 0.0;
+        R.bound_gap = 0.0;
+        R.iterations = R.bound_evals = R.point_evals = R.next_counter = R.fr_n = R.max_fr = 0;
+        R.n_pending = 0;
+        R.n_pushed = 0;
+        if (blockIdx.x == 0) trace_point(a, 0, -1);
+    }
+    __syncthreads();
+    while (!R.done) {
+        const int mode = R.mode, par = R.parity;
+        const double lo = R.lo, hi = R.hi, c = R.c;
+        const double den_lo = R.den_lo, den_c = R.den_c, den_hi = R.den_hi;
+        const long long it = R.iterations;
+        unsigned long long *acc = st->acc[par];
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Top);
+        btrace_point(a, it, 0);
 
-        // phase 1: every event, three warps (lo, centre, hi); point image at
-        // the centre, segment images of both children (root: of the root)
+        // event phase: every event, three warps (lo, centre, hi); point image
+        // at the centre, segment images of both children (root: of the
+        // root); short segments in the lane, long ones spread over the warp
         unsigned long long v[3] = {0, 0, 0};
         AtomicSink sa{a.A}, sb{a.B};
-        for (long long i = gtid; i < a.n; i += gsz) {
-            const double x = __ldg(a.xc + i), y = __ldg(a.yc + i), t = __ldg(a.t + i);
-            const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
-            const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
-            const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
-            const long long p = floor_bin(wc.x, wc.y, W, H);
-            if (p >= 0) {
-                atomicAdd(a.P + p, 1u);
-                v[0]++;
+        for (long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
+             base < a.n; base += gsz) {
+            const long long i = base + lane;
+            int cA = 0, cB = 0, dummy = 0;
+            if (i < a.n) {
+                const double x = __ldg(a.xc + i), y = __ldg(a.yc + i), t = __ldg(a.t + i);
+                const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
+                const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
+                const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
+                const long long p = floor_bin(wc.x, wc.y, W, H);
+                if (p >= 0) {
+                    atomicAdd(a.P + p, 1u);
+                    v[0]++;
+                }
+                if (mode == kModeRoot) {
+                    v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                    cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq.d[2 * lane], sa, dummy);
+                } else {
+                    v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
+                    cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq.d[2 * lane], sa, dummy);
+                    v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
+                    cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq.d[2 * lane + 1], sb,
+                                          dummy);
+                }
             }
-            if (mode == kModeRoot) {
-                v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                raster_segment(wl.x, wl.y, wh.x, wh.y, W, H, sa);
-            } else {
-                v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                raster_segment(wl.x, wl.y, wc.x, wc.y, W, H, sa);
-                v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                raster_segment(wc.x, wc.y, wh.x, wh.y, W, H, sb);
-            }
+            if (__any_sync(0xffffffffu, (cA | cB) != 0)) warp_drain(wq, cA, cB, W, H, a.A, a.B);
         }
-        block_add_u64<3>(v, (unsigned long long *)st->acc);
-        grid_barrier(bar, [] {});
+        __syncthreads();
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Events);
+        trace_max(a, it, kTrEventsMax);
+        btrace_point(a, it, 1);
+        block_add_u64<3>(v, acc);
+        grid_sync(ctr, target);
+        bclock(a, it, 4);
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels0);
 
-        // phase 2: contrast subtrees of the point image, exact sums of squares
-        // of both segment images; every image is left zeroed
-        const double mu = ddiv((double)st->acc[0], (double)a.tree.M);
-        for (int cut = blockIdx.x; cut < a.tree.C; cut += gridDim.x) {
-            const double r = eval_cut(a.tree, cut, SqU32Clear{a.P, mu}, scratch);
-            if (threadIdx.x == 0) a.tree.cutval[cut] = r;
+        // pixel phase: contrast subtrees of the point image, exact sums of
+        // squares of both segment images; every image is left zeroed
+        if (threadIdx.x == 0) {
+            if (blockIdx.x == 0) {
+                for (int k = 0; k < R.n_pending; k++) entry_store(a.fr + R.pend_idx[k], R.pend[k]);
+                unsigned long long *nxt = st->acc[par ^ 1];
+                for (int k = 0; k < 8; k++) __stcg(nxt + k, 0ull);
+            }
+            R.fiA = __ldcg(acc + 1);  // final after barrier 1; prefetch for the step
+            R.fiB = __ldcg(acc + 2);
+            R.p2A = __ldg(a.pow2 + R.fiA);
+            R.p2B = __ldg(a.pow2 + R.fiB);
         }
+        bclock(a, it, 5);
+        const double mu = ddiv((double)__ldcg(acc), (double)tree.M);
+        for (int cut = blockIdx.x, q = 0; cut < tree.C; cut += gridDim.x, q++) {
+            const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{a.P, mu}}, scratch);
+            if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
+        }
+        bclock(a, it, 6);
         unsigned long long w[2] = {0, 0};
-        for (long long p = gtid; p < a.tree.M; p += gsz) {
+        for (long long p = gtid; p < tree.M; p += gsz) {
             const unsigned long long ha = __ldcg(a.A + p), hb = __ldcg(a.B + p);
             if (ha) { w[0] += ha * ha; a.A[p] = 0u; }
             if (hb) { w[1] += hb * hb; a.B[p] = 0u; }
         }
-        block_add_u64<2>(w, (unsigned long long *)st->acc + 3);
-        grid_barrier(bar, [&] { leader_step(a, scratch); });
+        bclock(a, it, 7);
+        block_add_u64<2>(w, acc + 3);
+        bclock(a, it, 8);
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels1);
+        trace_max(a, it, kTrPixelsMax);
+        btrace_point(a, it, 2);
+        grid_sync(ctr, target);
+        bclock(a, it, 9);
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Step0);
+
+        // step: every block stages the cut sums, this node's bound integers and
+        // the frontier, finishes the contrast and takes the same BnB step
+        const long long n0 = R.fr_n;
+        for (int i = threadIdx.x; i < tree.C; i += blockDim.x) scratch[i] = __ldcg(tree.cutval + i);
+        if (n0 <= kFrView)
+            for (long long i = threadIdx.x; i < n0; i += blockDim.x) view[i] = entry_load(a.fr + i);
+        if (threadIdx.x == 0) {
+            R.sA = __ldcg(acc + 3);
+            R.sB = __ldcg(acc + 4);
+        }
+        __syncthreads();
+        bclock(a, it, 10);
+        const double S = top_combine(tree, scratch);
+        bclock(a, it, 11);
+        bnb_step(a, R, S, view);
+        bclock(a, it, 12);
+        if (threadIdx.x == 0) R.parity = par ^ 1;
+        if (blockIdx.x == 0) trace_point(a, it, kTrB0Step1);
+        btrace_point(a, it, 3);
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->nu_hat = R.nu_hat;
+        st->c_hat = R.c_hat;
+        st->bound_gap = R.bound_gap;
+        st->iterations = R.iterations;
+        st->bound_evals = R.bound_evals;
+        st->point_evals = R.point_evals;
+        st->fr_n = R.fr_n;
+        st->max_fr = R.max_fr;
+        st->next_counter = R.next_counter;
+        st->status = R.status;
+        st->done = 1;
     }
 }
 
+
 // ---------------------------------------------------------------- launchers
+constexpr size_t kBoundSmem = sizeof(WarpQueue) * (kThreads / 32);
+constexpr size_t kSolveSmem = kSolveSmemBytes;
+
+static bool g_attrs = false;
+static void set_attrs()
+{
+    if (g_attrs) return;
+    cudaFuncSetAttribute(k_bound_image, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBoundSmem);
+    cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem);
+    g_attrs = true;
+}
+
 void launch_center(const double *x, const double *y, long long n, double cx, double cy,
                    double *xc, double *yc, cudaStream_t s)
 {
@@ -460,8 +838,9 @@ void launch_bound_image(const double *xc, const double *yc, const double *t, lon
                         int W, int H, unsigned int *img, unsigned long long *acc,
                         cudaStream_t s)
 {
-    k_bound_image<<<event_blocks(n), kThreads, 0, s>>>(xc, yc, t, n, lo, den_lo, hi, den_hi, cx,
-                                                       cy, W, H, img, acc);
+    set_attrs();
+    k_bound_image<<<event_blocks(n), kThreads, kBoundSmem, s>>>(xc, yc, t, n, lo, den_lo, hi,
+                                                                den_hi, cx, cy, W, H, img, acc);
 }
 
 void launch_image_sums(const unsigned int *img, long long m, unsigned long long *acc,
@@ -484,18 +863,20 @@ void launch_contrast_f64(const double *img, double mu, const TreeDev &tree, doub
     k_contrast_top<<<1, kThreads, 0, s>>>(tree, out);
 }
 
-void launch_raster_segments(const double *segs, int k, int W, int H, unsigned int *counts,
-                            cudaStream_t s)
+void launch_raster_segments(const double *segs, int k, int W, int H, int chunk,
+                            unsigned int *counts, cudaStream_t s)
 {
-    k_raster_segments<<<(k + 127) / 128, 128, 0, s>>>(segs, k, W, H, counts);
+    k_raster_segments<<<(k + 127) / 128, 128, 0, s>>>(segs, k, W, H, chunk < 1 ? kChunk : chunk,
+                                                      counts);
 }
 
 int solve_block_threads() { return kSolveThreads; }
 
 int solve_grid_blocks(int device)
 {
+    set_attrs();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kSolveThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kSolveThreads, kSolveSmem);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm < 1) per_sm = 1;
@@ -504,10 +885,11 @@ int solve_grid_blocks(int device)
 
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s)
 {
+    set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
     return cudaLaunchCooperativeKernel((const void *)k_solve, dim3(blocks), dim3(kSolveThreads),
-                                       params, 0, s);
+                                       params, kSolveSmem, s);
 }
 
 }  // namespace evd

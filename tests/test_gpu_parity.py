@@ -30,13 +30,15 @@ def test_native_library_is_loaded():
 
 
 # ------------------------------------------------------------------ raster
-def test_segments_match_reference(seg_golden):
+@pytest.mark.parametrize("chunk", [0, 1, 2, 3, 7])
+def test_segments_match_reference(seg_golden, chunk):
+    """Every chunk size (seams between lanes) gives the reference's pixel sets."""
     by_dims = {}
     for seg, dims, cells in golden_segment_sets(seg_golden):
         by_dims.setdefault(dims, []).append((seg, cells))
     bad = 0
     for (w, h), items in by_dims.items():
-        got = con.rasterize_segments([s for s, _ in items], SensorGeometry(w, h))
+        got = con.rasterize_segments([s for s, _ in items], SensorGeometry(w, h), chunk=chunk)
         bad += sum(g != c for g, (_, c) in zip(got, items))
     assert bad == 0
 

@@ -1,0 +1,98 @@
+"""Per-iteration device timeline of one evd_solve (globaltimer trace).
+
+python tools/trace_solve.py [cfg] [repeats] [--all]
+Per node evaluation (us, from block 0's start of the node):
+  b0ev  block 0's events      maxev  the slowest block's events
+  bar1  last events -> block 0 leaves barrier 1
+  px    block 0's pixels      maxpx  the slowest block's pixels
+  bar2  last pixels -> block 0 leaves barrier 2
+  step  block 0's BnB step    total  node to node
+"""
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2209_13168_b200 as evd  # noqa: E402
+from paper_2209_13168_b200 import _lib, solver as sol, synth  # noqa: E402
+
+SLOTS = 8
+
+
+def trace(ctx):
+    buf = np.zeros(1 + SLOTS * (1 << 14), dtype=np.int64)
+    n = np.zeros(1, dtype=np.int64)
+    rc = ctx.lib.evd_solve_trace(ctx.h, _lib.ptr(buf, _lib._i64p), buf.size,
+                                 _lib.ptr(n, _lib._i64p))
+    assert rc == 0
+    return buf[: int(n[0])]
+
+
+def main():
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    cfg = int(args[0]) if args else 2
+    reps = int(args[1]) if len(args) > 1 else 3
+    b = synth.config_window(cfg)
+    for _ in range(reps):
+        r, st = sol.solve_window(b, evd.SolverParams())
+    tr = trace(_lib.context())
+    k = (len(tr) - 1) // SLOTS
+    T = tr[1:1 + SLOTS * k].reshape(k, SLOTS).astype(np.float64) / 1e3
+    k = min(k, st.point_evals)
+    cols = {
+        "b0ev": T[:k, 1] - T[:k, 0],
+        "maxev": T[:k, 2] - T[:k, 0],
+        "bar1": T[:k, 3] - T[:k, 2],
+        "px": T[:k, 4] - T[:k, 3],
+        "maxpx": T[:k, 5] - T[:k, 3],
+        "bar2": T[:k, 6] - T[:k, 5],
+        "step": T[:k, 7] - T[:k, 6],
+        "total": np.r_[T[1:k, 0] - T[:k - 1, 0], np.nan],
+    }
+    print(f"cfg {cfg}: n={b.n} iterations={r.iterations} device_ms={st.device_ms:.3f}")
+    print("node " + " ".join(f"{c:>8s}" for c in cols))
+    show = range(k) if "--all" in sys.argv else list(range(min(k, 12))) + list(range(max(12, k - 6), k))
+    for i in show:
+        print(f"{i:4d} " + " ".join(f"{cols[c][i]:8.1f}" for c in cols))
+    nar = slice(k // 2, k - 1)
+    print("median over the narrow half: " +
+          " ".join(f"{c}={np.nanmedian(v[nar]):.1f}" for c, v in cols.items()))
+    print("sum: " + " ".join(f"{c}={np.nansum(v):.0f}" for c, v in cols.items()))
+
+
+if __name__ == "__main__":
+    main()
+
+
+def block_trace(ctx, it_list=(40, 50, 80)):
+    S = 16
+    blocks = (_lib._i32 * 1)()
+    buf = np.zeros(128 * 2048 * S, dtype=np.int64)
+    ctx.lib.evd_solve_block_trace(ctx.h, _lib.ptr(buf, _lib._i64p), buf.size, blocks)
+    G = blocks[0]
+    raw = buf[: 128 * G * S].reshape(128, G, S)
+    bt = raw[:, :, :4].astype(np.float64) / 1e3
+    for it in it_list:
+        t0 = bt[it, 0, 0]
+        start = bt[it, :, 0] - t0
+        ev = bt[it, :, 1] - bt[it, :, 0]
+        px = bt[it, :, 2] - bt[it, :, 1]
+        step = bt[it, :, 3] - bt[it, :, 2]
+        print(f"node {it}: start skew p50/max {np.median(start):.1f}/{start.max():.1f} us; "
+              f"events p50/p90/max {np.median(ev):.1f}/{np.percentile(ev, 90):.1f}/{ev.max():.1f} "
+              f"(argmax block {int(ev.argmax())}); px+bar1 p50/max {np.median(px):.1f}/{px.max():.1f}; "
+              f"step+bar2 p50/max {np.median(step):.1f}/{step.max():.1f}")
+        c = raw[it, :, 4:13].astype(np.float64)
+        names = ["mu/acc", "cuts", "A/B px", "blkadd", "->bar2", "stage", "top", "bnb"]
+        d = np.diff(c, axis=1)
+        med = np.median(d, axis=0)
+        print("   block cycles (median over blocks): " +
+              " ".join(f"{n}={v:.0f}" for n, v in zip(names, med)))
+
+
+if "--blocks" in sys.argv:
+    block_trace(_lib.context())
