@@ -232,6 +232,17 @@ def run_gpu(args, rank, world, local):
         if os.path.exists(tfile):
             with open(tfile) as fh:
                 traffic = json.load(fh).get("k_solve_dram_bytes")
+        # atomic roofline: every pixel increment is one L2 RED; peak measured by
+        # tools/bench_atomics.cu for this image size (profiles/atomic_peak.json)
+        atomic = None
+        afile = os.path.join(ROOT, "profiles", "atomic_peak.json")
+        if os.path.exists(afile):
+            with open(afile) as fh:
+                apk = json.load(fh).get("random_m89960_gatomics_per_s")
+            ach = res.marks / (k_ms / 1e3) / 1e9
+            atomic = {"achieved": ach, "peak": apk, "unit": "G atomics/s",
+                      "frac": ach / apk if apk else None, "marks_per_solve": int(res.marks),
+                      "peak_source": "tools/bench_atomics.cu (u32 RED, random pixels, M=89960)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
@@ -242,9 +253,10 @@ def run_gpu(args, rank, world, local):
             "solve": {"nu": res.nu, "contrast": res.contrast, "bound_gap": res.bound_gap,
                       "iterations": res.iterations, "bound_evals": res.bound_evals,
                       "point_evals": res.point_evals, "max_frontier": res.max_frontier,
-                      "kernel_ms": k_ms},
+                      "marks": int(res.marks), "kernel_ms": k_ms},
+            "atomic_roofline": atomic,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n,
-                    "d2h_bytes_per_step": 200},  # SolveState read back (evd_internal.h)
+                    "d2h_bytes_per_step": 272},  # SolveState read back (evd_internal.h)
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "roofline": {"bound": "hbm", "kernel": "k_solve", "achieved": achieved,
@@ -269,7 +281,7 @@ def run_gpu(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")

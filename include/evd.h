@@ -113,6 +113,7 @@ typedef struct {
     int64_t point_evals;  /* contrast_at evaluations */
     int64_t max_frontier; /* largest live queue */
     double device_ms;     /* device time of the solve (CUDA events on the ctx stream) */
+    uint64_t marks;       /* pixel increments made in all images (atomic work) */
 } evd_solve_result;
 
 /* Whole solve on the device for the resident window (one cooperative

@@ -49,7 +49,8 @@ class SolveResult(ctypes.Structure):
     _fields_ = [("nu", ctypes.c_double), ("contrast", ctypes.c_double),
                 ("bound_gap", ctypes.c_double), ("iterations", ctypes.c_int64),
                 ("bound_evals", ctypes.c_int64), ("point_evals", ctypes.c_int64),
-                ("max_frontier", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+                ("max_frontier", ctypes.c_int64), ("device_ms", ctypes.c_double),
+                ("marks", ctypes.c_uint64)]
 
 
 _d = ctypes.POINTER(ctypes.c_double)

@@ -716,6 +716,7 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
         res->bound_evals = st.bound_evals;
         res->point_evals = st.point_evals;
         res->max_frontier = st.max_fr;
+        res->marks = st.marks;
         res->device_ms = ms;
         ctx->trace_n = 1 + kTraceSlots * std::min<long long>(st.iterations + 1, kTraceIters);
         if (st.status == kStatusIterLimit)

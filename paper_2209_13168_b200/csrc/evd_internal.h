@@ -41,12 +41,14 @@ struct SolveState {
     double lo, hi, c, den_lo, den_c, den_hi;
     int mode, done;
     // per-node accumulators, double-buffered by node parity: 0 in_image,
-    // 1 fully_inside A, 2 fully_inside B, 3 S_bar A, 4 S_bar B
+    // 1 fully_inside A, 2 fully_inside B, 3 segment marks, 4 S_bar A, 5 S_bar B,
+    // 7 event work counter
     unsigned long long acc[2][8];
     // incumbent and diagnostics
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
     int status, pad;
+    unsigned long long marks;  // pixel increments of all images over the solve
 };
 
 struct SolveArgs {

@@ -255,8 +255,10 @@ struct SqF64 {
 
 // Evaluate cut subtree c of the pairwise tree with the whole block; returns
 // the subtree sum to every thread.
+__device__ __forceinline__ void bclock(const SolveArgs &a, long long it, int k);
 template <class Q>
-__device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc)
+__device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc,
+                           const SolveArgs &dbg_a, long long dbg_it)
 {
     const int l0 = T.cut_leaf0[c], nl = T.cut_leaf0[c + 1] - l0;
     const int j = threadIdx.x & 7, ngroups = blockDim.x >> 3;
@@ -265,7 +267,9 @@ __device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc)
         const double v = pairwise_leaf8(lf.x, lf.y, j, q);
         if (j == 0) loc[i] = v;
     }
+    if (dbg_a.btrace) bclock(dbg_a, dbg_it, 14);
     __syncthreads();
+    if (dbg_a.btrace) bclock(dbg_a, dbg_it, 15);
     const int t0 = T.cut_trip0[c], ni = T.cut_trip0[c + 1] - t0;
     const int *lvl = T.cut_lvl + (long long)c * (kMaxLevels + 1);
     const int nlev = T.cut_nlev[c];
@@ -303,14 +307,14 @@ __global__ void k_contrast_cuts_u32(const unsigned int *img, const unsigned long
 {
     __shared__ double loc[kCutSmem];
     const double mu = ddiv((double)*in_image, (double)T.M);  // EventImage.mean, contrast.py:35-36
-    const double r = eval_cut(T, blockIdx.x, SqU32{img, mu}, loc);
+    const double r = eval_cut(T, blockIdx.x, SqU32{img, mu}, loc, SolveArgs{}, 0);
     if (threadIdx.x == 0) T.cutval[blockIdx.x] = r;
 }
 
 __global__ void k_contrast_cuts_f64(const double *img, double mu, TreeDev T)
 {
     __shared__ double loc[kCutSmem];
-    const double r = eval_cut(T, blockIdx.x, SqF64{img, mu}, loc);
+    const double r = eval_cut(T, blockIdx.x, SqF64{img, mu}, loc, SolveArgs{}, 0);
     if (threadIdx.x == 0) T.cutval[blockIdx.x] = r;
 }
 
@@ -410,6 +414,7 @@ struct Replica {
     int mode, done, status, parity;
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
+    unsigned long long marks;  // pixel increments of all images over the solve
     // this node's integer accumulators and pow(fi/M, 2) table values
     unsigned long long fiA, fiB, sA, sB;
     double p2A, p2B;
@@ -666,6 +671,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
         R.c_hat = 0.0;
         R.bound_gap = 0.0;
         R.iterations = R.bound_evals = R.point_evals = R.next_counter = R.fr_n = R.max_fr = 0;
+        R.marks = 0;
         R.n_pending = 0;
         R.n_pushed = 0;
         if (blockIdx.x == 0) trace_point(a, 0, -1);
@@ -683,10 +689,12 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
         // event phase: every event, three warps (lo, centre, hi); point image
         // at the centre, segment images of both children (root: of the
         // root); short segments in the lane, long ones spread over the warp
-        unsigned long long v[3] = {0, 0, 0};
+        unsigned long long v[4] = {0, 0, 0, 0};
         AtomicSink sa{a.A}, sb{a.B};
-        for (long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
-             base < a.n; base += gsz) {
+        // first round static, then warps take batches of 32 events from a
+        // per-node work counter (acc[7]), so blocks finish together
+        long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
+        while (base < a.n) {
             const long long i = base + lane;
             int cA = 0, cB = 0, dummy = 0;
             if (i < a.n) {
@@ -710,13 +718,18 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
                                           dummy);
                 }
             }
-            if (__any_sync(0xffffffffu, (cA | cB) != 0)) warp_drain(wq, cA, cB, W, H, a.A, a.B);
+            if (__any_sync(0xffffffffu, (cA | cB) != 0))
+                dummy += warp_drain(wq, cA, cB, W, H, a.A, a.B);
+            v[3] += dummy;
+            long long nb = 0;
+            if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+            base = __shfl_sync(0xffffffffu, nb, 0);
         }
         __syncthreads();
         if (blockIdx.x == 0) trace_point(a, it, kTrB0Events);
         trace_max(a, it, kTrEventsMax);
         btrace_point(a, it, 1);
-        block_add_u64<3>(v, acc);
+        block_add_u64<4>(v, acc);
         grid_sync(ctr, target);
         bclock(a, it, 4);
         if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels0);
@@ -736,8 +749,10 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
         }
         bclock(a, it, 5);
         const double mu = ddiv((double)__ldcg(acc), (double)tree.M);
+        bclock(a, it, 13);
         for (int cut = blockIdx.x, q = 0; cut < tree.C; cut += gridDim.x, q++) {
-            const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{a.P, mu}}, scratch);
+            const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{a.P, mu}}, scratch,
+                                      a, it);
             if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
         }
         bclock(a, it, 6);
@@ -748,7 +763,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             if (hb) { w[1] += hb * hb; a.B[p] = 0u; }
         }
         bclock(a, it, 7);
-        block_add_u64<2>(w, acc + 3);
+        block_add_u64<2>(w, acc + 4);
         bclock(a, it, 8);
         if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels1);
         trace_max(a, it, kTrPixelsMax);
@@ -764,8 +779,9 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
         if (n0 <= kFrView)
             for (long long i = threadIdx.x; i < n0; i += blockDim.x) view[i] = entry_load(a.fr + i);
         if (threadIdx.x == 0) {
-            R.sA = __ldcg(acc + 3);
-            R.sB = __ldcg(acc + 4);
+            R.sA = __ldcg(acc + 4);
+            R.sB = __ldcg(acc + 5);
+            R.marks += __ldcg(acc + 0) + __ldcg(acc + 3);
         }
         __syncthreads();
         bclock(a, it, 10);
@@ -787,6 +803,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
         st->point_evals = R.point_evals;
         st->fr_n = R.fr_n;
         st->max_fr = R.max_fr;
+        st->marks = R.marks;
         st->next_counter = R.next_counter;
         st->status = R.status;
         st->done = 1;

@@ -92,6 +92,10 @@ def block_trace(ctx, it_list=(40, 50, 80)):
         med = np.median(d, axis=0)
         print("   block cycles (median over blocks): " +
               " ".join(f"{n}={v:.0f}" for n, v in zip(names, med)))
+        e = raw[it, :, 13:16].astype(np.float64)
+        pre = e[:, 0] - raw[it, :, 5]
+        print("   cut detail: mu=%.0f leaves=%.0f sync=%.0f" % (
+            np.median(pre), np.median(e[:, 1] - e[:, 0]), np.median(e[:, 2] - e[:, 1])))
 
 
 if "--blocks" in sys.argv:
