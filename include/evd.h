@@ -84,6 +84,13 @@ int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k
                      uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks,
                      uint32_t *counts);
 
+/* Batched frontier: bound_terms (contrast.py:241-251) for k intervals in one
+ * pass over the resident window (events held in registers across groups of
+ * consecutive intervals; adjacent intervals sharing an endpoint share its
+ * warp).  Same outputs as evd_bound_images without images. */
+int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
+                      uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks);
+
 /* image_contrast (contrast.py:61-64) of a caller image: np.sum((c - mean)**2)/M
  * with numpy's pairwise summation order; mean = in_image / m. */
 int evd_image_contrast(evd_ctx *ctx, const double *counts, int64_t m, int64_t in_image,

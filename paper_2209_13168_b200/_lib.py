@@ -23,7 +23,8 @@ EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
 SYMBOLS = (
     "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
     "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
-    "evd_point_images", "evd_bound_images", "evd_image_contrast", "evd_rasterize_segments",
+    "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
+    "evd_rasterize_segments",
     "evd_solve", "evd_solve_trace", "evd_solve_block_trace", "evd_pow2_table",
 )
 
@@ -74,6 +75,7 @@ _SIGS = {
     "evd_warp_scale": (ctypes.c_int, [_vp, _d, _i64, _f64, _f64, _d]),
     "evd_point_images": (ctypes.c_int, [_vp, _d, _i32, _i64p, _d, _u32p]),
     "evd_bound_images": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p, _u32p]),
+    "evd_eval_frontier": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p]),
     "evd_image_contrast": (ctypes.c_int, [_vp, _d, _i64, _i64, _d]),
     "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _i32, _u32p]),
     "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),

@@ -187,3 +187,24 @@ def bound_terms(batch: EventBatch, interval: VelocityInterval) -> ContrastBound:
     """Contrast upper bound over the interval (contrast.py:241-251)."""
     s_bar, fi, _, _ = bound_terms_many(batch, [interval.lo], [interval.hi])
     return assemble_bound(int(s_bar[0]), int(fi[0]), batch.geometry.n_pixels)
+
+
+def frontier_terms(batch: EventBatch, lo, hi, ctx=None, loaded=False):
+    """Batched frontier: exact bound integers for k intervals in one pass.
+
+    Same values as ``bound_terms_many`` (s_bar uint64[k], fully_inside int64[k],
+    marks uint64[k]); the whole frontier is evaluated by one evd_eval_frontier
+    call (SURVEY §8(a) part 4).
+    """
+    lo, hi = _lib.f64(np.atleast_1d(lo)), _lib.f64(np.atleast_1d(hi))
+    ctx = ctx if loaded else load_window(batch, ctx)
+    k = lo.size
+    s_bar = np.empty(k, dtype=np.uint64)
+    fi = np.empty(k, dtype=np.int64)
+    marks = np.empty(k, dtype=np.uint64)
+    rc = ctx.lib.evd_eval_frontier(ctx.h, _lib.ptr(lo), _lib.ptr(hi), k,
+                                   _lib.ptr(s_bar, _lib._u64p), _lib.ptr(fi, _lib._i64p),
+                                   _lib.ptr(marks, _lib._u64p))
+    if rc:
+        _raise(ctx, rc)
+    return s_bar, fi, marks

@@ -74,7 +74,9 @@ struct evd_ctx {
     DevBuf<unsigned long long> acc;    // 8 accumulators
     DevBuf<double> dscratch;           // misc device doubles
     DevBuf<double> wx, wy, wt, wxo, wyo;
-    DevBuf<double> segs;
+    DevBuf<double> segs, fargs;
+    DevBuf<unsigned int> fimg;          // batched-frontier images (kept zeroed)
+    DevBuf<unsigned long long> facc;
     DevBuf<unsigned int> seg_counts;
     TreePlan tree;
     // bound assembly table pow(f/M, 2)
@@ -396,6 +398,9 @@ void evd_destroy(evd_ctx *ctx)
     for (DevBuf<double> *b : {&ctx->xc, &ctx->yc, &ctx->t, &ctx->dscratch, &ctx->wx, &ctx->wy,
                               &ctx->wt, &ctx->wxo, &ctx->wyo, &ctx->segs, &ctx->pow2})
         b->release();
+    ctx->fargs.release();
+    ctx->fimg.release();
+    ctx->facc.release();
     ctx->img.release();
     ctx->seg_counts.release();
     ctx->acc.release();
@@ -581,6 +586,59 @@ int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k
         if (fully_inside) fully_inside[j] = (int64_t)h[0];
         if (marks) marks[j] = h[2];
         if (s_bar) s_bar[j] = h[3];
+    }
+    return EVD_OK;
+}
+
+int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
+                      uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    if (k < 0) return fail(ctx, EVD_ERR_ARG, "negative interval count");
+    if (k == 0) return EVD_OK;
+    const long long M = (long long)ctx->W * ctx->H;
+    std::vector<double> host(4 * (size_t)k);
+    for (int j = 0; j < k; j++) {
+        if (lo[j] > hi[j]) return fail(ctx, EVD_ERR_ARG, "empty interval [%.17g, %.17g]", lo[j], hi[j]);
+        if ((rc = check_den(ctx, lo[j], ctx->tau, &host[2 * (size_t)k + j]))) return rc;
+        if ((rc = check_den(ctx, hi[j], ctx->tau, &host[3 * (size_t)k + j]))) return rc;
+        host[j] = lo[j];
+        host[(size_t)k + j] = hi[j];
+    }
+    CU(cudaSetDevice(ctx->device));
+    // images of up to kb intervals at a time (kept zeroed between calls)
+    const long long cap_bytes = 8ll << 30;
+    long long kb = std::max<long long>(1, cap_bytes / (M * 4));
+    kb = std::min<long long>(kb, k);
+    kb = (kb + kFrontGroupHost - 1) / kFrontGroupHost * kFrontGroupHost;
+    if ((long long)ctx->fimg.cap < kb * M) {
+        CU(ctx->fimg.ensure((size_t)(kb * M)));
+        CU(cudaMemsetAsync(ctx->fimg.p, 0, ctx->fimg.cap * sizeof(unsigned int), ctx->stream));
+    }
+    CU(ctx->fargs.ensure(4 * (size_t)k));
+    CU(ctx->facc.ensure(3 * (size_t)k));
+    CU(cudaMemcpyAsync(ctx->fargs.p, host.data(), host.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemsetAsync(ctx->facc.p, 0, 3 * (size_t)k * sizeof(unsigned long long), ctx->stream));
+    const double *d_lo = ctx->fargs.p, *d_hi = d_lo + k, *d_dl = d_lo + 2 * k, *d_dh = d_lo + 3 * k;
+    unsigned long long *f_fi = ctx->facc.p, *f_ms = f_fi + k;  // fi[k], then (marks, s_bar)[k]
+    for (long long j0 = 0; j0 < k; j0 += kb) {
+        const int kk = (int)std::min<long long>(kb, k - j0);
+        launch_frontier(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, d_lo + j0, d_hi + j0, d_dl + j0,
+                        d_dh + j0, kk, ctx->W / 2.0, ctx->H / 2.0, ctx->W, ctx->H, ctx->fimg.p, M,
+                        f_fi + j0, f_ms + 2 * j0, ctx->stream);
+        LAUNCHED(2);
+    }
+    std::vector<unsigned long long> out(3 * (size_t)k);
+    CU(cudaMemcpyAsync(out.data(), ctx->facc.p, out.size() * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < k; j++) {
+        if (fully_inside) fully_inside[j] = (int64_t)out[j];
+        if (marks) marks[j] = out[(size_t)k + 2 * j];
+        if (s_bar) s_bar[j] = out[(size_t)k + 2 * j + 1];
     }
     return EVD_OK;
 }

@@ -101,6 +101,12 @@ void launch_bound_image(const double *xc, const double *yc, const double *t, lon
                         double lo, double den_lo, double hi, double den_hi, double cx, double cy,
                         int W, int H, unsigned int *img, unsigned long long *acc,
                         cudaStream_t s);
+void launch_frontier(const double *xc, const double *yc, const double *t, long long n,
+                     const double *lo, const double *hi, const double *den_lo,
+                     const double *den_hi, int K, double cx, double cy, int W, int H,
+                     unsigned int *images, long long M, unsigned long long *fi_out,
+                     unsigned long long *marks_s, cudaStream_t s);
+constexpr int kFrontGroupHost = 32;
 void launch_image_sums(const unsigned int *img, long long m, unsigned long long *acc,
                        cudaStream_t s);
 void launch_contrast_u32(const unsigned int *img, const unsigned long long *in_image,

@@ -49,6 +49,7 @@ struct AtomicSink {
 // Per-warp queue of built segments: lane l owns slots 2l, 2l+1.
 struct WarpQueue {
     SegDesc d[64];
+    unsigned int *img[64];  // image each queued segment marks
     int off[33];  // exclusive prefix of chunk counts per lane
     int na[32];   // chunks of the lane's first segment
 };
@@ -56,9 +57,9 @@ struct WarpQueue {
 // Build one segment; sample it in the lane when it has at most one crossing,
 // otherwise queue it in the lane's shared-memory slot for warp_drain.
 // Returns the number of queued chunks.
-template <class Sink>
 __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
-                                                int H, SegDesc &slot, Sink &sink, int &marks)
+                                                int H, WarpQueue &q, int slot, AtomicSink &sink,
+                                                int &marks)
 {
     SegDesc d;
     const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
@@ -67,15 +68,15 @@ __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx,
         marks += sample_chunk(d, 0, W, H, sink);
         return 0;
     }
-    slot = d;
+    q.d[slot] = d;
+    q.img[slot] = sink.img;
     return c;
 }
 
 // Sample every chunk the warp queued, in rounds of 32: all lanes position
 // their cursors together, then step one item per iteration; chunks hold
 // nearly equal item counts, so the lanes stay converged.
-__device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H,
-                                          unsigned int *imgA, unsigned int *imgB)
+__device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H)
 {
     const int lane = threadIdx.x & 31;
     int incl = cA + cB;
@@ -95,7 +96,7 @@ __device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, i
         bool active = false;
         int slot = 0;
         Cursor c;
-        AtomicSink sink{imgA};
+        AtomicSink sink{nullptr};
         if (t < total) {
             int L = 0;  // largest lane with off[L] <= t
 #pragma unroll
@@ -104,7 +105,7 @@ __device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, i
             const int r = t - q.off[L];
             const bool second = r >= q.na[L];
             slot = 2 * L + (second ? 1 : 0);
-            if (second) sink.img = imgB;
+            sink.img = q.img[slot];
             active = cursor_init(q.d[slot], second ? r - q.na[L] : r, c);
         }
         while (__any_sync(0xffffffffu, active))
@@ -187,12 +188,91 @@ __global__ void __launch_bounds__(kThreads) k_bound_image(
             const Warped a = warp_event(x, y, tt, lo, den_lo, cx, cy);
             const Warped b = warp_event(x, y, tt, hi, den_hi, cx, cy);
             v[0] += fully_inside(a.x, a.y, b.x, b.y, W, H);
-            c = segment_or_queue(a.x, a.y, b.x, b.y, W, H, wq.d[2 * lane], sink, marks);
+            c = segment_or_queue(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, marks);
         }
-        if (__any_sync(0xffffffffu, c != 0)) marks += warp_drain(wq, c, 0, W, H, img, img);
+        if (__any_sync(0xffffffffu, c != 0)) marks += warp_drain(wq, c, 0, W, H);
         v[1] += marks;
     }
     block_add_u64<2>(v, acc);
+}
+
+// ---------------------------------------------------------------- batched frontier
+// bound_terms (contrast.py:241-251) for K intervals in one launch.  Lane j of
+// a warp owns interval k0 + j of a group of 32 consecutive intervals and the
+// warp walks events one at a time: every lane evaluates the same event (a
+// broadcast load) at its own interval, so the 32 segments are neighbours along
+// one trajectory and take the same branches.  An interval whose lower
+// endpoint is its left neighbour's upper endpoint takes that warp by shuffle.
+// Per-interval fully_inside / marks stay in registers; blocks are ordered
+// group-major so a group's 32 images stay in L2 while it is in flight.
+constexpr int kFrontGroup = 32;
+
+__global__ void __launch_bounds__(kThreads) k_frontier(
+    const double *__restrict__ xc, const double *__restrict__ yc, const double *__restrict__ t,
+    long long n, const double *__restrict__ lo, const double *__restrict__ hi,
+    const double *__restrict__ den_lo, const double *__restrict__ den_hi, int K, double cx,
+    double cy, int W, int H, unsigned int *images, long long M, int bpg,
+    unsigned long long *fi_out)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    __shared__ unsigned long long s_fi[kFrontGroup];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int g = blockIdx.x / bpg, tb = blockIdx.x % bpg;
+    const int k = g * kFrontGroup + lane;
+    const bool valid = k < K;
+    const int kc = valid ? k : K - 1;
+    const double my_lo = __ldg(lo + kc), my_hi = __ldg(hi + kc);
+    const double my_dlo = __ldg(den_lo + kc), my_dhi = __ldg(den_hi + kc);
+    const double left_hi = __shfl_up_sync(0xffffffffu, my_hi, 1);
+    const bool shared_lo = lane > 0 && my_lo == left_hi;
+    unsigned int *img = images + (long long)kc * M;
+    AtomicSink sink{img};
+    if (threadIdx.x < kFrontGroup) s_fi[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long fi = 0;
+    const long long gw = (long long)tb * wpb + warp, nw = (long long)bpg * wpb;
+    for (long long e = gw; e < n; e += nw) {
+        const double x = __ldg(xc + e), y = __ldg(yc + e), tt = __ldg(t + e);
+        const Warped b = warp_event(x, y, tt, my_hi, my_dhi, cx, cy);
+        Warped a;
+        a.x = __shfl_up_sync(0xffffffffu, b.x, 1);
+        a.y = __shfl_up_sync(0xffffffffu, b.y, 1);
+        if (!shared_lo) a = warp_event(x, y, tt, my_lo, my_dlo, cx, cy);
+        int c = 0, m = 0;
+        if (valid) {
+            fi += fully_inside(a.x, a.y, b.x, b.y, W, H);
+            c = segment_or_queue(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
+        }
+        if (__any_sync(0xffffffffu, c != 0)) warp_drain(wq, c, 0, W, H);
+    }
+    if (valid && fi) atomicAdd(s_fi + lane, fi);
+    __syncthreads();
+    if (threadIdx.x < kFrontGroup && g * kFrontGroup + (int)threadIdx.x < K) {
+        const int kk = g * kFrontGroup + threadIdx.x;
+        if (s_fi[threadIdx.x]) atomicAdd(fi_out + kk, s_fi[threadIdx.x]);
+    }
+}
+
+// marks = sum(H_bar) (upper_bound_image().in_image_events) and S_bar =
+// sum(H_bar^2) per interval image (exact u64), leaving the images zeroed.
+// marks_s points at [marks_k, s_bar_k] pairs.
+__global__ void k_frontier_sums(unsigned int *images, long long M, int bpi,
+                                unsigned long long *marks_s)
+{
+    const int k = blockIdx.x / bpi, part = blockIdx.x % bpi;
+    unsigned int *img = images + (long long)k * M;
+    unsigned long long v[2] = {0, 0};
+    for (long long p = part * (long long)blockDim.x + threadIdx.x; p < M;
+         p += (long long)bpi * blockDim.x) {
+        const unsigned long long h = __ldcs(img + p);
+        if (h) {
+            v[0] += h;
+            v[1] += h * h;
+            img[p] = 0u;
+        }
+    }
+    block_add_u64<2>(v, marks_s + 2 * k);
 }
 
 // acc[0] += sum(img), acc[1] += sum(img^2) -- exact integers (contrast.py:238,249)
@@ -709,17 +789,17 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
                 }
                 if (mode == kModeRoot) {
                     v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                    cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq.d[2 * lane], sa, dummy);
+                    cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
                 } else {
                     v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                    cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq.d[2 * lane], sa, dummy);
+                    cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
                     v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                    cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq.d[2 * lane + 1], sb,
+                    cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb,
                                           dummy);
                 }
             }
             if (__any_sync(0xffffffffu, (cA | cB) != 0))
-                dummy += warp_drain(wq, cA, cB, W, H, a.A, a.B);
+                dummy += warp_drain(wq, cA, cB, W, H);
             v[3] += dummy;
             long long nb = 0;
             if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
@@ -821,6 +901,8 @@ static void set_attrs()
     if (g_attrs) return;
     cudaFuncSetAttribute(k_bound_image, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBoundSmem);
+    cudaFuncSetAttribute(k_frontier, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBoundSmem);
     cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem);
     g_attrs = true;
 }
@@ -858,6 +940,24 @@ void launch_bound_image(const double *xc, const double *yc, const double *t, lon
     set_attrs();
     k_bound_image<<<event_blocks(n), kThreads, kBoundSmem, s>>>(xc, yc, t, n, lo, den_lo, hi,
                                                                 den_hi, cx, cy, W, H, img, acc);
+}
+
+void launch_frontier(const double *xc, const double *yc, const double *t, long long n,
+                     const double *lo, const double *hi, const double *den_lo,
+                     const double *den_hi, int K, double cx, double cy, int W, int H,
+                     unsigned int *images, long long M, unsigned long long *fi_out,
+                     unsigned long long *marks_s, cudaStream_t s)
+{
+    set_attrs();
+    const int groups = (K + kFrontGroup - 1) / kFrontGroup;
+    long long bpg = (n + kThreads - 1) / kThreads;
+    if (bpg > (long long)num_sms() * 4) bpg = (long long)num_sms() * 4;
+    if (bpg < 1) bpg = 1;
+    k_frontier<<<(unsigned)(groups * bpg), kThreads, kBoundSmem, s>>>(
+        xc, yc, t, n, lo, hi, den_lo, den_hi, K, cx, cy, W, H, images, M, (int)bpg, fi_out);
+    long long bpi = (M + kThreads * 4 - 1) / (kThreads * 4);
+    if (bpi < 1) bpi = 1;
+    k_frontier_sums<<<(unsigned)(K * bpi), kThreads, 0, s>>>(images, M, (int)bpi, marks_s);
 }
 
 void launch_image_sums(const unsigned int *img, long long m, unsigned long long *acc,
