@@ -128,9 +128,28 @@ typedef struct {
  * when max_iterations is reached. */
 int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res);
 
-/* Device timestamps (ns, %globaltimer) of the last evd_solve: out[0] = start,
- * then for node evaluation i (0 = root): out[1+2i] = every event binned,
- * out[2+2i] = every pixel reduced.  *n receives the number of valid entries. */
+/* Many windows in one launch (estimate_stream_divergence, solver.py:139-162):
+ * window w is events [offsets[w], offsets[w+1]) of the resident event set
+ * (evd_set_events with all windows concatenated; they share width, height,
+ * tau).  The CTAs are split into `groups` independent solvers (0 = auto) that
+ * take windows round-robin; each window is solved exactly as evd_solve.
+ * results[w].status: EVD_OK, EVD_ERR_ITER_LIMIT (incumbent in the record),
+ * or EVD_ERR_NO_EVENTS for an empty window. */
+typedef struct {
+    double nu, contrast, bound_gap;
+    int64_t iterations, bound_evals, point_evals, max_frontier;
+    uint64_t marks;
+    int32_t status;
+    int32_t groups;   /* solver groups the launch used */
+} evd_window_result;
+
+int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, int32_t groups,
+                      const evd_solve_params *params, evd_window_result *results,
+                      double *device_ms);
+
+/* Device timestamps (ns, %globaltimer) of the last solve (first window of
+ * group 0): out[0] = start, then 8 slots per node evaluation (see
+ * csrc/evd_internal.h TraceSlot).  *n receives the number of valid entries. */
 int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n);
 
 /* Per-block timestamps of the first 128 node evaluations of the last

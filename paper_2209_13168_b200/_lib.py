@@ -25,7 +25,8 @@ SYMBOLS = (
     "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
     "evd_rasterize_segments",
-    "evd_solve", "evd_solve_trace", "evd_solve_block_trace", "evd_pow2_table",
+    "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
+    "evd_pow2_table",
 )
 
 
@@ -54,6 +55,14 @@ class SolveResult(ctypes.Structure):
                 ("marks", ctypes.c_uint64)]
 
 
+class WindowResult(ctypes.Structure):
+    _fields_ = [("nu", ctypes.c_double), ("contrast", ctypes.c_double),
+                ("bound_gap", ctypes.c_double), ("iterations", ctypes.c_int64),
+                ("bound_evals", ctypes.c_int64), ("point_evals", ctypes.c_int64),
+                ("max_frontier", ctypes.c_int64), ("marks", ctypes.c_uint64),
+                ("status", ctypes.c_int32), ("groups", ctypes.c_int32)]
+
+
 _d = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _u64p = ctypes.POINTER(ctypes.c_uint64)
@@ -79,6 +88,8 @@ _SIGS = {
     "evd_image_contrast": (ctypes.c_int, [_vp, _d, _i64, _i64, _d]),
     "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _i32, _u32p]),
     "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
+    "evd_solve_windows": (ctypes.c_int, [_vp, _i64p, _i32, _i32, ctypes.POINTER(SolveParams),
+                                         ctypes.POINTER(WindowResult), _d]),
     "evd_solve_trace": (ctypes.c_int, [_vp, _i64p, _i64, _i64p]),
     "evd_solve_block_trace": (ctypes.c_int, [_vp, _i64p, _i64, ctypes.POINTER(_i32)]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),

@@ -70,7 +70,8 @@ struct evd_ctx {
     double tau = 0.0;
     DevBuf<double> xc, yc, t;
     // scratch
-    DevBuf<unsigned int> img;          // 3 images (P, A, B)
+    DevBuf<unsigned int> img;          // 3 images (P, A, B) of the per-call entry points
+    DevBuf<unsigned int> simg;         // solve images, per group (always left zeroed)
     DevBuf<unsigned long long> acc;    // 8 accumulators
     DevBuf<double> dscratch;           // misc device doubles
     DevBuf<double> wx, wy, wt, wxo, wyo;
@@ -86,6 +87,9 @@ struct evd_ctx {
     DevBuf<SolveState> state;
     DevBuf<FrontierEntry> frontier;
     DevBuf<GridBar> bar;
+    DevBuf<unsigned long long> bar2;   // per-group barrier counters
+    DevBuf<long long> woff;            // window offsets
+    DevBuf<WindowResult> wres;
     DevBuf<long long> trace, btrace;
     long long trace_n = 0;
     int solve_blocks = 0;
@@ -402,11 +406,15 @@ void evd_destroy(evd_ctx *ctx)
     ctx->fimg.release();
     ctx->facc.release();
     ctx->img.release();
+    ctx->simg.release();
     ctx->seg_counts.release();
     ctx->acc.release();
     ctx->state.release();
     ctx->frontier.release();
     ctx->bar.release();
+    ctx->bar2.release();
+    ctx->woff.release();
+    ctx->wres.release();
     TreePlan &tp = ctx->tree;
     tp.leaves.release();
     tp.cut_leaf0.release();
@@ -683,14 +691,17 @@ int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t 
     return EVD_OK;
 }
 
-int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res)
+}  // extern "C"
+
+namespace {
+
+// Run the device-resident BnB over n_windows windows of the resident events
+// (window w = events [off[w], off[w+1])) with `groups` independent CTA groups.
+static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
+                       const evd_solve_params *params, std::vector<WindowResult> &out,
+                       float *ms_out)
 {
-    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
-    if (!params || !res) return fail(ctx, EVD_ERR_ARG, "params/result is NULL");
-    int rc = need_events(ctx);
-    if (rc) return rc;
-    memset(res, 0, sizeof *res);
-    if (ctx->n == 0) return fail(ctx, EVD_ERR_NO_EVENTS, "no events in batch");
+    int rc;
     if (!(params->gamma > 0.0)) return fail(ctx, EVD_ERR_ARG, "gamma must be positive");
     const double tau = ctx->tau, eps = params->epsilon;
     if (!(eps >= 0.0 && eps < 1.0)) return fail(ctx, EVD_ERR_ARG, "epsilon must be in [0, 1)");
@@ -703,46 +714,59 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
     const long long M = (long long)ctx->W * ctx->H;
     CU(cudaSetDevice(ctx->device));
     if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
-    const int blocks = ctx->solve_blocks;
-    if ((rc = ensure_tree(ctx, M, blocks))) return rc;
-    if ((rc = ensure_pow2(ctx, M, ctx->n))) return rc;
-    CU(ctx->img.ensure(3 * M));
-    CU(ctx->state.ensure(1));
-    CU(ctx->bar.ensure(1));
+    groups = std::max(1, std::min(groups, ctx->solve_blocks));
+    const int GB = ctx->solve_blocks / groups;
+    long long max_n = 0;
+    for (int w = 0; w < n_windows; w++) max_n = std::max(max_n, off[w + 1] - off[w]);
+    if ((rc = ensure_tree(ctx, M, GB))) return rc;
+    if ((rc = ensure_pow2(ctx, M, max_n))) return rc;
+    CU(ctx->tree.cutval.ensure((size_t)ctx->tree.dev.C * groups));
+    ctx->tree.dev.cutval = ctx->tree.cutval.p;
+    if (ctx->simg.cap < (size_t)(3 * M * groups)) {  // the kernel leaves them zeroed
+        CU(ctx->simg.ensure((size_t)(3 * M * groups)));
+        CU(cudaMemsetAsync(ctx->simg.p, 0, ctx->simg.cap * sizeof(unsigned int), ctx->stream));
+    }
+    CU(ctx->state.ensure(groups));
+    CU(ctx->bar2.ensure(2 * (size_t)groups));
     CU(ctx->trace.ensure(1 + kTraceSlots * kTraceIters));
     CU(ctx->btrace.ensure((size_t)kBTraceIters * kBTraceMaxBlocks * kBTraceSlots));
-        CU(cudaMemsetAsync(ctx->trace.p, 0, (1 + kTraceSlots * kTraceIters) * sizeof(long long), ctx->stream));
-    long long cap = (long long)ctx->frontier.cap;
-    if (cap < 4096) cap = 4096;
+    CU(cudaMemsetAsync(ctx->trace.p, 0, (1 + kTraceSlots * kTraceIters) * sizeof(long long),
+                       ctx->stream));
+    CU(ctx->woff.ensure(n_windows + 1));
+    CU(ctx->wres.ensure(n_windows));
+    CU(cudaMemcpyAsync(ctx->woff.p, off, (n_windows + 1) * sizeof(long long),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    long long cap = std::max<long long>(4096, (long long)(ctx->frontier.cap / groups));
     const long long need = params->max_iterations + 2;
     if (need > 0 && need < cap) cap = need;
+    out.assign(n_windows, WindowResult{});
+    std::vector<int> todo(n_windows);
+    for (int w = 0; w < n_windows; w++) todo[w] = w;
+    float total_ms = 0.f;
     while (true) {
-        CU(ctx->frontier.ensure((size_t)cap));
-        SolveState st{};
-        st.lo = lo0;
-        st.hi = hi0;
-        st.c = c0;
-        st.den_lo = den_lo;
-        st.den_c = den_c;
-        st.den_hi = den_hi;
-        st.mode = kModeRoot;
-        st.bound_gap = 0.0;
-        CU(cudaMemcpyAsync(ctx->state.p, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemsetAsync(ctx->bar.p, 0, sizeof(GridBar), ctx->stream));
-        CU(cudaMemsetAsync(ctx->img.p, 0, 3 * M * sizeof(unsigned int), ctx->stream));
+        CU(ctx->frontier.ensure((size_t)(cap * groups)));
+        CU(cudaMemsetAsync(ctx->bar2.p, 0, 2 * groups * sizeof(unsigned long long), ctx->stream));
+        CU(cudaMemsetAsync(ctx->wres.p, 0, n_windows * sizeof(WindowResult), ctx->stream));
         SolveArgs a{};
         a.xc = ctx->xc.p;
         a.yc = ctx->yc.p;
         a.t = ctx->t.p;
-        a.n = ctx->n;
+        a.offsets = ctx->woff.p;
+        a.n_windows = n_windows;
+        a.groups = groups;
+        a.group_blocks = GB;
         a.W = ctx->W;
         a.H = ctx->H;
         a.cx = ctx->W / 2.0;
         a.cy = ctx->H / 2.0;
         a.tau = tau;
-        a.P = ctx->img.p;
-        a.A = ctx->img.p + M;
-        a.B = ctx->img.p + 2 * M;
+        a.lo0 = lo0;
+        a.hi0 = hi0;
+        a.c0 = c0;
+        a.den_lo0 = den_lo;
+        a.den_c0 = den_c;
+        a.den_hi0 = den_hi;
+        a.img = ctx->simg.p;
         a.tree = ctx->tree.dev;
         a.pow2 = ctx->pow2.p;
         a.gamma = params->gamma;
@@ -750,39 +774,111 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
         a.max_iter = params->max_iterations;
         a.st = ctx->state.p;
         a.fr = ctx->frontier.p;
-        a.fr_cap = (long long)ctx->frontier.cap;
-        a.bar = ctx->bar.p;
+        a.fr_cap = cap;
+        a.bar = ctx->bar2.p;
+        a.res = ctx->wres.p;
         a.trace = ctx->trace.p;
         a.trace_iters = kTraceIters;
         a.btrace = ctx->btrace.p;
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU(launch_solve(a, blocks, ctx->stream));
+        CU(launch_solve(a, groups * GB, ctx->stream));
         LAUNCHED(1);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
-        CU(cudaMemcpyAsync(&st, ctx->state.p, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<WindowResult> got(n_windows);
+        CU(cudaMemcpyAsync(got.data(), ctx->wres.p, n_windows * sizeof(WindowResult),
+                           cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        if (st.status == kStatusCapacity) {
-            cap *= 8;
-            continue;
+        total_ms += ms;
+        bool again = false;
+        for (int w : todo) {
+            out[w] = got[w];
+            if (got[w].status == kStatusCapacity) again = true;
         }
-        res->nu = st.nu_hat;
-        res->contrast = st.c_hat;
-        res->bound_gap = st.bound_gap;
-        res->iterations = st.iterations;
-        res->bound_evals = st.bound_evals;
-        res->point_evals = st.point_evals;
-        res->max_frontier = st.max_fr;
-        res->marks = st.marks;
-        res->device_ms = ms;
-        ctx->trace_n = 1 + kTraceSlots * std::min<long long>(st.iterations + 1, kTraceIters);
-        if (st.status == kStatusIterLimit)
-            return fail(ctx, EVD_ERR_ITER_LIMIT,
-                        "iteration limit reached after %lld iterations (best nu=%.17g, contrast=%.17g)",
-                        st.iterations, st.nu_hat, st.c_hat);
-        return EVD_OK;
+        if (!again) break;
+        cap *= 8;  // frontier outgrew its buffer: rerun (the solve is deterministic)
     }
+    ctx->trace_n = 1 + kTraceSlots * std::min<long long>(out[0].iterations + 1, kTraceIters);
+    if (ms_out) *ms_out = total_ms;
+    return EVD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !res) return fail(ctx, EVD_ERR_ARG, "params/result is NULL");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    memset(res, 0, sizeof *res);
+    if (ctx->n == 0) return fail(ctx, EVD_ERR_NO_EVENTS, "no events in batch");
+    const long long off[2] = {0, ctx->n};
+    std::vector<WindowResult> out;
+    float ms = 0.f;
+    if ((rc = run_windows(ctx, off, 1, 1, params, out, &ms))) return rc;
+    const WindowResult &w = out[0];
+    res->nu = w.nu;
+    res->contrast = w.contrast;
+    res->bound_gap = w.bound_gap;
+    res->iterations = w.iterations;
+    res->bound_evals = w.bound_evals;
+    res->point_evals = w.point_evals;
+    res->max_frontier = w.max_fr;
+    res->marks = w.marks;
+    res->device_ms = ms;
+    if (w.status == kStatusIterLimit)
+        return fail(ctx, EVD_ERR_ITER_LIMIT,
+                    "iteration limit reached after %lld iterations (best nu=%.17g, contrast=%.17g)",
+                    w.iterations, w.nu, w.contrast);
+    return EVD_OK;
+}
+
+int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, int32_t groups,
+                      const evd_solve_params *params, evd_window_result *results,
+                      double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !results || !offsets || n_windows < 0)
+        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_windows arguments");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    if (n_windows == 0) return EVD_OK;
+    if (offsets[0] < 0 || offsets[n_windows] > ctx->n)
+        return fail(ctx, EVD_ERR_ARG, "window offsets outside the resident events");
+    for (int w = 0; w < n_windows; w++)
+        if (offsets[w + 1] < offsets[w]) return fail(ctx, EVD_ERR_ARG, "offsets must be non-decreasing");
+    if (groups <= 0) {  // auto: ~2 events per thread per group, at least one window per group
+        long long tot = offsets[n_windows] - offsets[0];
+        const double avg = (double)tot / n_windows;
+        if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
+        const int per = std::max(1, (int)std::ceil(avg / (2.0 * solve_block_threads())));
+        groups = std::max(1, std::min(n_windows, ctx->solve_blocks / per));
+    }
+    std::vector<WindowResult> out;
+    float ms = 0.f;
+    if ((rc = run_windows(ctx, (const long long *)offsets, n_windows, groups, params, out, &ms)))
+        return rc;
+    for (int w = 0; w < n_windows; w++) {
+        evd_window_result &r = results[w];
+        r.nu = out[w].nu;
+        r.contrast = out[w].contrast;
+        r.bound_gap = out[w].bound_gap;
+        r.iterations = out[w].iterations;
+        r.bound_evals = out[w].bound_evals;
+        r.point_evals = out[w].point_evals;
+        r.max_frontier = out[w].max_fr;
+        r.marks = out[w].marks;
+        r.status = out[w].status == kStatusOk ? EVD_OK
+                   : out[w].status == kStatusIterLimit ? EVD_ERR_ITER_LIMIT
+                   : out[w].status == kStatusEmpty ? EVD_ERR_NO_EVENTS : EVD_ERR_CUDA;
+        r.groups = groups;
+    }
+    if (device_ms) *device_ms = ms;
+    return EVD_OK;
 }
 
 int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n)

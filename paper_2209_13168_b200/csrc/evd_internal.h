@@ -51,23 +51,36 @@ struct SolveState {
     unsigned long long marks;  // pixel increments of all images over the solve
 };
 
+// Result of one window of evd_solve_windows / evd_solve.
+enum WindowStatus : int { kStatusEmpty = 3 };
+struct WindowResult {
+    double nu, contrast, bound_gap;
+    long long iterations, bound_evals, point_evals, max_fr;
+    unsigned long long marks;
+    int status, pad;
+};
+
 struct SolveArgs {
-    const double *xc, *yc, *t;
-    long long n;
+    const double *xc, *yc, *t;   // centred events of all windows, concatenated
+    const long long *offsets;     // [n_windows + 1] window w = [offsets[w], offsets[w+1])
+    int n_windows;
+    int groups, group_blocks;     // independent solver groups x CTAs per group
     int W, H;
     double cx, cy, tau;
-    unsigned int *P, *A, *B;  // point image, two child segment images (u32, zeroed)
-    TreeDev tree;
-    const double *pow2;       // pow(fi / M, 2.0) via host libm, fi in [0, n]
+    double lo0, hi0, c0, den_lo0, den_c0, den_hi0;  // root domain (host arithmetic)
+    unsigned int *img;            // per group: P, A, B (u32, M each, zeroed)
+    TreeDev tree;                 // cut plan for group_blocks CTAs; cutval: C per group
+    const double *pow2;           // pow(fi / M, 2.0) via host libm, fi in [0, max n]
     double gamma, min_width;
     long long max_iter;
-    SolveState *st;
-    FrontierEntry *fr;
+    SolveState *st;               // per group (accumulators)
+    FrontierEntry *fr;            // per group, fr_cap entries each
     long long fr_cap;
-    void *bar;                // GridBar
-    long long *trace;         // [1 + kTraceSlots*trace_iters] globaltimer ns
+    unsigned long long *bar;      // per group: barrier counter (stride 2)
+    WindowResult *res;            // per window
+    long long *trace;             // [1 + kTraceSlots*trace_iters] globaltimer ns (group 0, window 0)
     long long trace_iters;
-    long long *btrace;        // [kBTraceIters][gridDim][4] per-block timestamps (or null)
+    long long *btrace;            // [kBTraceIters][group_blocks][kBTraceSlots] (or null)
 };
 
 constexpr int kBTraceIters = 128;

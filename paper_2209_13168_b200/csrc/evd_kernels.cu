@@ -441,20 +441,22 @@ __device__ __forceinline__ void trace_max(const SolveArgs &a, long long it, int 
 __device__ __forceinline__ void btrace_point(const SolveArgs &a, long long it, int k)
 {
     if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
-    a.btrace[(it * gridDim.x + blockIdx.x) * kBTraceSlots + k] = globaltimer();
+    a.btrace[(it * a.group_blocks + blockIdx.x) * kBTraceSlots + k] = globaltimer();
 }
 // sub-phase markers (SM cycles) in slots 4.. of the block trace
 __device__ __forceinline__ void bclock(const SolveArgs &a, long long it, int k)
 {
     if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
-    a.btrace[(it * gridDim.x + blockIdx.x) * kBTraceSlots + k] = clock64();
+    a.btrace[(it * a.group_blocks + blockIdx.x) * kBTraceSlots + k] = clock64();
 }
 
-// Grid barrier on a monotone 64-bit arrival counter (no reset round trip):
-// the n-th barrier completes when the counter reaches n * gridDim.x.
-__device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long long &target)
+// Barrier over a solver group of `blocks` CTAs on a monotone 64-bit arrival
+// counter (no reset round trip): the n-th barrier completes when the counter
+// reaches n * blocks.
+__device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long long &target,
+                                          int blocks)
 {
-    target += gridDim.x;
+    target += blocks;
     __syncthreads();
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
@@ -530,7 +532,8 @@ __device__ __forceinline__ void replica_push(const SolveArgs &a, Replica &R, lon
 // with >=, the iteration cap, then the best-first pop and stop test of the
 // next iteration.  Whole block; identical in every block.  Frontier entries
 // [0, fr_n) are in `view` when fr_n <= kFrView (else read from global).
-__device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const FrontierEntry *view)
+__device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const FrontierEntry *view,
+                         FrontierEntry *fr)
 {
     const long long n0 = R.fr_n;
     const bool staged = n0 <= kFrView;
@@ -573,7 +576,7 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
     }
     auto entry = [&](long long i) -> FrontierEntry {
         if (i >= n0) return R.pushed[i - n0];
-        return staged ? view[i] : entry_load(a.fr + i);
+        return staged ? view[i] : entry_load(fr + i);
     };
     // best-first pop: argmax over the committed entries and this step's pushes
     __shared__ double r_b[32];
@@ -585,7 +588,7 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
         long long c;
         if (i >= n0) { b = R.pushed[i - n0].bound; c = R.pushed[i - n0].counter; }
         else if (staged) { b = view[i].bound; c = view[i].counter; }
-        else { b = __ldcg(&a.fr[i].bound); c = __ldcg(&a.fr[i].counter); }
+        else { b = __ldcg(&fr[i].bound); c = __ldcg(&fr[i].counter); }
         if (bi < 0 || better(b, c, bb, bc)) { bb = b; bc = c; bi = i; }
     }
 #pragma unroll
@@ -645,18 +648,18 @@ struct TreeCache {
     int top_lvl[kMaxLevels + 1];
 };
 
-// Returns a TreeDev whose cut index q means global cut blockIdx.x + q*gridDim.x
+// Returns a TreeDev whose cut index q means global cut gb + q*GB
 // (local = true), or the global tables when they do not fit (local = false).
-__device__ TreeDev cache_tree(const TreeDev &g, TreeCache &tc, bool &local)
+__device__ TreeDev cache_tree(const TreeDev &g, TreeCache &tc, bool &local, int gb, int GB)
 {
     __shared__ int s_ok, s_nq;
     if (threadIdx.x == 0) {
-        int nq = g.C > (int)blockIdx.x ? (g.C - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        int nq = g.C > gb ? (g.C - 1 - gb) / GB + 1 : 0;
         int ok = nq <= kCacheCuts && g.top_lvl[g.top_levels] <= kCacheTop &&
                  g.top_levels <= kMaxLevels;
         int nl = 0, nt = 0;
         for (int q = 0; ok && q < nq; q++) {
-            const int c = blockIdx.x + q * gridDim.x;
+            const int c = gb + q * GB;
             tc.cut_leaf0[q] = nl;
             tc.cut_trip0[q] = nt;
             nl += g.cut_leaf0[c + 1] - g.cut_leaf0[c];
@@ -674,7 +677,7 @@ __device__ TreeDev cache_tree(const TreeDev &g, TreeCache &tc, bool &local)
     if (!local) return g;  // does not fit: read the global tables
     const int nq = s_nq;
     for (int q = 0; q < nq; q++) {
-        const int c = blockIdx.x + q * gridDim.x;
+        const int c = gb + q * GB;
         const int l0 = g.cut_leaf0[c], nl = g.cut_leaf0[c + 1] - l0;
         const int t0 = g.cut_trip0[c], nt = g.cut_trip0[c + 1] - t0;
         for (int i = threadIdx.x; i < nl; i += blockDim.x) tc.leaves[tc.cut_leaf0[q] + i] = g.leaves[l0 + i];
@@ -727,169 +730,195 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
     FrontierEntry *view = reinterpret_cast<FrontierEntry *>(smem + kCutSmem * sizeof(double));
     TreeCache &tc = *reinterpret_cast<TreeCache *>(smem + kRegionA);
     __shared__ Replica R;
-    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(a.bar);
+    // this CTA's solver group: an independent solver over group_blocks CTAs
+    const int GB = a.group_blocks;
+    const int grp = blockIdx.x / GB, gb = blockIdx.x % GB;
+    if (grp >= a.groups) return;
+    const bool tracer = grp == 0;
+    unsigned long long *ctr = a.bar + 2 * grp;
     unsigned long long target = 0;
-    SolveState *st = a.st;
+    SolveState *st = a.st + grp;
+    FrontierEntry *fr = a.fr + (long long)grp * a.fr_cap;
+    const long long M = a.tree.M;
+    unsigned int *P = a.img + (long long)grp * 3 * M, *A = P + M, *B = A + M;
     const int lane = threadIdx.x & 31;
-    const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long gsz = (long long)gridDim.x * blockDim.x;
+    const long long gtid = gb * (long long)blockDim.x + threadIdx.x;
+    const long long gsz = (long long)GB * blockDim.x;
     const int W = a.W, H = a.H;
     bool local_cuts;
-    const TreeDev tree = cache_tree(a.tree, tc, local_cuts);
-    if (threadIdx.x == 0) {
-        R.lo = __ldcg(&st->lo);
-        R.hi = __ldcg(&st->hi);
-        R.c = __ldcg(&st->c);
-        R.den_lo = __ldcg(&st->den_lo);
-        R.den_c = __ldcg(&st->den_c);
-        R.den_hi = __ldcg(&st->den_hi);
-        R.mode = kModeRoot;
-        R.done = 0;
-        R.status = kStatusOk;
-        R.parity = 0;
-        R.nu_hat = 0.0;
-        R.c_hat = 0.0;
-        R.bound_gap = 0.0;
-        R.iterations = R.bound_evals = R.point_evals = R.next_counter = R.fr_n = R.max_fr = 0;
-        R.marks = 0;
-        R.n_pending = 0;
-        R.n_pushed = 0;
-        if (blockIdx.x == 0) trace_point(a, 0, -1);
-    }
-    __syncthreads();
-    while (!R.done) {
-        const int mode = R.mode, par = R.parity;
-        const double lo = R.lo, hi = R.hi, c = R.c;
-        const double den_lo = R.den_lo, den_c = R.den_c, den_hi = R.den_hi;
-        const long long it = R.iterations;
-        unsigned long long *acc = st->acc[par];
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Top);
-        btrace_point(a, it, 0);
+    TreeDev gtree = a.tree;
+    gtree.cutval = a.tree.cutval + (long long)grp * a.tree.C;
+    const TreeDev tree = cache_tree(gtree, tc, local_cuts, gb, GB);
+    if (tracer && gb == 0) trace_point(a, 0, -1);
 
-        // event phase: every event, three warps (lo, centre, hi); point image
-        // at the centre, segment images of both children (root: of the
-        // root); short segments in the lane, long ones spread over the warp
-        unsigned long long v[4] = {0, 0, 0, 0};
-        AtomicSink sa{a.A}, sb{a.B};
-        // first round static, then warps take batches of 32 events from a
-        // per-node work counter (acc[7]), so blocks finish together
-        long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
-        while (base < a.n) {
-            const long long i = base + lane;
-            int cA = 0, cB = 0, dummy = 0;
-            if (i < a.n) {
-                const double x = __ldg(a.xc + i), y = __ldg(a.yc + i), t = __ldg(a.t + i);
-                const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
-                const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
-                const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
-                const long long p = floor_bin(wc.x, wc.y, W, H);
-                if (p >= 0) {
-                    atomicAdd(a.P + p, 1u);
-                    v[0]++;
-                }
-                if (mode == kModeRoot) {
-                    v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                    cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
-                } else {
-                    v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                    cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
-                    v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                    cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb,
-                                          dummy);
-                }
-            }
-            if (__any_sync(0xffffffffu, (cA | cB) != 0))
-                dummy += warp_drain(wq, cA, cB, W, H);
-            v[3] += dummy;
-            long long nb = 0;
-            if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
-            base = __shfl_sync(0xffffffffu, nb, 0);
+    for (int w = grp; w < a.n_windows; w += a.groups) {
+        const long long off = a.offsets[w], n = a.offsets[w + 1] - off;
+        if (n == 0) {
+            if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
+            continue;
         }
-        __syncthreads();
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Events);
-        trace_max(a, it, kTrEventsMax);
-        btrace_point(a, it, 1);
-        block_add_u64<4>(v, acc);
-        grid_sync(ctr, target);
-        bclock(a, it, 4);
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels0);
-
-        // pixel phase: contrast subtrees of the point image, exact sums of
-        // squares of both segment images; every image is left zeroed
+        const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
+        // fresh accumulators for the window: every CTA is past the previous
+        // window's last step before block 0 clears them
+        grid_sync(ctr, target, GB);
+        if (gb == 0 && threadIdx.x == 0) {
+            unsigned long long *z = &st->acc[0][0];
+            for (int k = 0; k < 16; k++) __stcg(z + k, 0ull);
+        }
+        grid_sync(ctr, target, GB);
         if (threadIdx.x == 0) {
-            if (blockIdx.x == 0) {
-                for (int k = 0; k < R.n_pending; k++) entry_store(a.fr + R.pend_idx[k], R.pend[k]);
-                unsigned long long *nxt = st->acc[par ^ 1];
-                for (int k = 0; k < 8; k++) __stcg(nxt + k, 0ull);
-            }
-            R.fiA = __ldcg(acc + 1);  // final after barrier 1; prefetch for the step
-            R.fiB = __ldcg(acc + 2);
-            R.p2A = __ldg(a.pow2 + R.fiA);
-            R.p2B = __ldg(a.pow2 + R.fiB);
+            R.lo = a.lo0;
+            R.hi = a.hi0;
+            R.c = a.c0;
+            R.den_lo = a.den_lo0;
+            R.den_c = a.den_c0;
+            R.den_hi = a.den_hi0;
+            R.mode = kModeRoot;
+            R.done = 0;
+            R.status = kStatusOk;
+            R.parity = 0;
+            R.nu_hat = 0.0;
+            R.c_hat = 0.0;
+            R.bound_gap = 0.0;
+            R.iterations = R.bound_evals = R.point_evals = R.next_counter = R.fr_n = R.max_fr = 0;
+            R.marks = 0;
+            R.n_pending = 0;
+            R.n_pushed = 0;
         }
-        bclock(a, it, 5);
-        const double mu = ddiv((double)__ldcg(acc), (double)tree.M);
-        bclock(a, it, 13);
-        for (int cut = blockIdx.x, q = 0; cut < tree.C; cut += gridDim.x, q++) {
-            const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{a.P, mu}}, scratch,
-                                      a, it);
-            if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
-        }
-        bclock(a, it, 6);
-        unsigned long long w[2] = {0, 0};
-        for (long long p = gtid; p < tree.M; p += gsz) {
-            const unsigned long long ha = __ldcg(a.A + p), hb = __ldcg(a.B + p);
-            if (ha) { w[0] += ha * ha; a.A[p] = 0u; }
-            if (hb) { w[1] += hb * hb; a.B[p] = 0u; }
-        }
-        bclock(a, it, 7);
-        block_add_u64<2>(w, acc + 4);
-        bclock(a, it, 8);
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Pixels1);
-        trace_max(a, it, kTrPixelsMax);
-        btrace_point(a, it, 2);
-        grid_sync(ctr, target);
-        bclock(a, it, 9);
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Step0);
+        __syncthreads();
+        while (!R.done) {
+            const int mode = R.mode, par = R.parity;
+            const double lo = R.lo, hi = R.hi, c = R.c;
+            const double den_lo = R.den_lo, den_c = R.den_c, den_hi = R.den_hi;
+            const long long it = R.iterations;
+            unsigned long long *acc = st->acc[par];
+            const bool tr = tracer && w == 0;
+            if (tr && gb == 0) trace_point(a, it, kTrB0Top);
+            if (tr) btrace_point(a, it, 0);
 
-        // step: every block stages the cut sums, this node's bound integers and
-        // the frontier, finishes the contrast and takes the same BnB step
-        const long long n0 = R.fr_n;
-        for (int i = threadIdx.x; i < tree.C; i += blockDim.x) scratch[i] = __ldcg(tree.cutval + i);
-        if (n0 <= kFrView)
-            for (long long i = threadIdx.x; i < n0; i += blockDim.x) view[i] = entry_load(a.fr + i);
-        if (threadIdx.x == 0) {
-            R.sA = __ldcg(acc + 4);
-            R.sB = __ldcg(acc + 5);
-            R.marks += __ldcg(acc + 0) + __ldcg(acc + 3);
+            // event phase: every event, three warps (lo, centre, hi); point
+            // image at the centre, segment images of both children (root: of
+            // the root); short segments in the lane, long ones spread over the
+            // warp.  First round static, then warps take batches of 32 events
+            // from the node's work counter (acc[7]) so CTAs finish together.
+            unsigned long long v[4] = {0, 0, 0, 0};
+            AtomicSink sa{A}, sb{B};
+            long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
+            while (base < n) {
+                const long long i = base + lane;
+                int cA = 0, cB = 0, dummy = 0;
+                if (i < n) {
+                    const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
+                    const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
+                    const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
+                    const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
+                    const long long p = floor_bin(wc.x, wc.y, W, H);
+                    if (p >= 0) {
+                        atomicAdd(P + p, 1u);
+                        v[0]++;
+                    }
+                    if (mode == kModeRoot) {
+                        v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                        cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
+                    } else {
+                        v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
+                        cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
+                        v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
+                        cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb,
+                                              dummy);
+                    }
+                }
+                if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain(wq, cA, cB, W, H);
+                v[3] += dummy;
+                long long nb = 0;
+                if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+                base = __shfl_sync(0xffffffffu, nb, 0);
+            }
+            __syncthreads();
+            if (tr && gb == 0) trace_point(a, it, kTrB0Events);
+            if (tr) trace_max(a, it, kTrEventsMax);
+            if (tr) btrace_point(a, it, 1);
+            block_add_u64<4>(v, acc);
+            grid_sync(ctr, target, GB);
+            if (tr) bclock(a, it, 4);
+            if (tr && gb == 0) trace_point(a, it, kTrB0Pixels0);
+
+            // pixel phase: contrast subtrees of the point image, exact sums of
+            // squares of both segment images; every image is left zeroed
+            if (threadIdx.x == 0) {
+                if (gb == 0) {
+                    for (int k = 0; k < R.n_pending; k++) entry_store(fr + R.pend_idx[k], R.pend[k]);
+                    unsigned long long *nxt = st->acc[par ^ 1];
+                    for (int k = 0; k < 8; k++) __stcg(nxt + k, 0ull);
+                }
+                R.fiA = __ldcg(acc + 1);  // final after barrier 1; prefetch for the step
+                R.fiB = __ldcg(acc + 2);
+            }
+            if (tr) bclock(a, it, 5);
+            const double mu = ddiv((double)__ldcg(acc), (double)tree.M);
+            if (tr) bclock(a, it, 13);
+            for (int cut = gb, q = 0; cut < tree.C; cut += GB, q++) {
+                const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{P, mu}}, scratch,
+                                          a, tr ? it : kBTraceIters);
+                if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
+            }
+            if (tr) bclock(a, it, 6);
+            unsigned long long ws[2] = {0, 0};
+            for (long long p = gtid; p < tree.M; p += gsz) {
+                const unsigned long long ha = __ldcg(A + p), hb = __ldcg(B + p);
+                if (ha) { ws[0] += ha * ha; A[p] = 0u; }
+                if (hb) { ws[1] += hb * hb; B[p] = 0u; }
+            }
+            if (threadIdx.x == 0) {  // pow(fi/M, 2) table values, needed by the step
+                R.p2A = __ldg(a.pow2 + R.fiA);
+                R.p2B = __ldg(a.pow2 + R.fiB);
+            }
+            if (tr) bclock(a, it, 7);
+            block_add_u64<2>(ws, acc + 4);
+            if (tr) bclock(a, it, 8);
+            if (tr && gb == 0) trace_point(a, it, kTrB0Pixels1);
+            if (tr) trace_max(a, it, kTrPixelsMax);
+            if (tr) btrace_point(a, it, 2);
+            grid_sync(ctr, target, GB);
+            if (tr) bclock(a, it, 9);
+            if (tr && gb == 0) trace_point(a, it, kTrB0Step0);
+
+            // step: every CTA stages the cut sums, this node's bound integers
+            // and the frontier, finishes the contrast and takes the same step
+            const long long n0 = R.fr_n;
+            for (int i = threadIdx.x; i < tree.C; i += blockDim.x) scratch[i] = __ldcg(tree.cutval + i);
+            if (n0 <= kFrView)
+                for (long long i = threadIdx.x; i < n0; i += blockDim.x) view[i] = entry_load(fr + i);
+            if (threadIdx.x == 0) {
+                R.sA = __ldcg(acc + 4);
+                R.sB = __ldcg(acc + 5);
+                R.marks += __ldcg(acc + 0) + __ldcg(acc + 3);
+            }
+            __syncthreads();
+            if (tr) bclock(a, it, 10);
+            const double S = top_combine(tree, scratch);
+            if (tr) bclock(a, it, 11);
+            bnb_step(a, R, S, view, fr);
+            if (tr) bclock(a, it, 12);
+            if (threadIdx.x == 0) R.parity = par ^ 1;
+            if (tr && gb == 0) trace_point(a, it, kTrB0Step1);
+            if (tr) btrace_point(a, it, 3);
+            __syncthreads();
         }
-        __syncthreads();
-        bclock(a, it, 10);
-        const double S = top_combine(tree, scratch);
-        bclock(a, it, 11);
-        bnb_step(a, R, S, view);
-        bclock(a, it, 12);
-        if (threadIdx.x == 0) R.parity = par ^ 1;
-        if (blockIdx.x == 0) trace_point(a, it, kTrB0Step1);
-        btrace_point(a, it, 3);
-        __syncthreads();
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        st->nu_hat = R.nu_hat;
-        st->c_hat = R.c_hat;
-        st->bound_gap = R.bound_gap;
-        st->iterations = R.iterations;
-        st->bound_evals = R.bound_evals;
-        st->point_evals = R.point_evals;
-        st->fr_n = R.fr_n;
-        st->max_fr = R.max_fr;
-        st->marks = R.marks;
-        st->next_counter = R.next_counter;
-        st->status = R.status;
-        st->done = 1;
+        if (gb == 0 && threadIdx.x == 0) {
+            WindowResult &r = a.res[w];
+            r.nu = R.nu_hat;
+            r.contrast = R.c_hat;
+            r.bound_gap = R.bound_gap;
+            r.iterations = R.iterations;
+            r.bound_evals = R.bound_evals;
+            r.point_evals = R.point_evals;
+            r.max_fr = R.max_fr;
+            r.marks = R.marks;
+            r.status = R.status;
+        }
     }
 }
-
 
 // ---------------------------------------------------------------- launchers
 constexpr size_t kBoundSmem = sizeof(WarpQueue) * (kThreads / 32);

@@ -10,9 +10,11 @@ result (nu, contrast, bound_gap, iterations) is the reference's, bit for bit.
 
 from __future__ import annotations
 
+import ctypes
 import logging
 import time
 from dataclasses import dataclass
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -140,9 +142,76 @@ def grid_search_oracle(batch: EventBatch, params: SolverParams, n_points: int
     return float(nus[best]), float(contrasts[best])
 
 
+def solve_windows(batches: list[EventBatch], params: SolverParams, groups: int = 0, ctx=None
+                  ) -> tuple[list, float, int]:
+    """Solve many windows in one device launch (evd_solve_windows).
+
+    All windows must share sensor geometry and tau (as batch_stream's do).
+    Returns ([WindowResult per window], device seconds, solver groups used).
+    Empty windows get status EVD_ERR_NO_EVENTS.
+    """
+    if not batches:
+        return [], 0.0, 0
+    g0, tau = batches[0].geometry, float(batches[0].tau)
+    if any(b.geometry.width != g0.width or b.geometry.height != g0.height or float(b.tau) != tau
+           for b in batches):
+        raise ValueError("solve_windows needs windows of one geometry and tau")
+    velocity_domain(tau, params.epsilon)
+    sizes = np.array([b.n for b in batches], dtype=np.int64)
+    offsets = np.zeros(len(batches) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    cat = lambda k: np.concatenate([np.asarray(getattr(b, k), dtype=np.float64) for b in batches])
+    ctx = load_window(SimpleNamespace(x=cat("x"), y=cat("y"), t=cat("t"), tau=tau, geometry=g0),
+                      ctx)
+    p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
+                         float(params.min_interval_width), int(params.max_iterations))
+    res = (_lib.WindowResult * len(batches))()
+    ms = (ctypes.c_double * 1)()
+    rc = ctx.lib.evd_solve_windows(ctx.h, _lib.ptr(offsets, _lib._i64p), len(batches),
+                                   int(groups), p, res, ms)
+    if rc:
+        _raise(ctx, rc)
+    return list(res), ms[0] / 1e3, (res[0].groups if len(batches) else 0)
+
+
 def estimate_stream_divergence(batches: list[EventBatch], params: SolverParams
                                ) -> list[DivergenceSample]:
-    """BnB per window; empty windows leave a gap (solver.py:139-162)."""
+    """BnB per window; empty windows leave a gap (solver.py:139-162).
+
+    All non-empty windows are solved in one device launch (evd_solve_windows)
+    when they share geometry and tau; each result equals maximise_contrast_bnb's.
+    ``runtime`` is the launch's wall time divided evenly over its windows.
+    """
+    live = [b for b in batches if b.n]
+    if not live:
+        return []
+    same = all(b.geometry.width == live[0].geometry.width and
+               b.geometry.height == live[0].geometry.height and b.tau == live[0].tau
+               for b in live)
+    if not same:
+        return _estimate_each(batches, params)
+    start = time.perf_counter()
+    results, _, _ = solve_windows(live, params)
+    per = (time.perf_counter() - start) / len(live)
+    samples = []
+    for batch, r in zip(live, results):
+        if r.status == _lib.EVD_ERR_ITER_LIMIT:
+            LOG.warning("batch at t=%.3f s: %s", batch.t_start,
+                        IterationLimitError(r.nu, r.contrast, int(r.iterations)))
+            continue
+        if r.status != _lib.EVD_OK:
+            raise _lib.EvdError(r.status, f"window at t={batch.t_start}: status {r.status}")
+        samples.append(DivergenceSample(
+            t=batch.t_end,
+            divergence=divergence_from_velocity(r.nu, batch.tau),
+            contrast=r.contrast,
+            bound_gap=r.bound_gap,
+            iterations=int(r.iterations),
+            runtime=per))
+    return samples
+
+
+def _estimate_each(batches: list[EventBatch], params: SolverParams) -> list[DivergenceSample]:
     samples = []
     for batch in batches:
         if batch.n == 0:

@@ -1,0 +1,64 @@
+"""Many windows per launch (evd_solve_windows) == one solve per window (GPU)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, f64
+import paper_2209_13168_b200 as evd
+from paper_2209_13168_b200 import _lib, solver as sol, synth
+from paper_2209_13168_b200.events import EventBatch, SensorGeometry
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(r, ref):
+    return (r.nu, r.contrast, r.bound_gap, int(r.iterations)) == (
+        f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
+
+
+@pytest.mark.parametrize("groups", [0, 1, 3, 7])
+def test_sequence_windows_match_reference(groups):
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        seq = json.load(fh)["sequence"]
+    batches = [synth.sequence_window(s["k"]) for s in seq]
+    res, secs, g = sol.solve_windows(batches, evd.SolverParams(), groups=groups)
+    assert secs > 0 and g >= 1
+    for r, s in zip(res, seq):
+        assert r.status == 0 and _same(r, s["result"]), (s["k"], r.nu)
+
+
+def test_small_windows_and_gaps(bnb_golden):
+    meta, windows = bnb_golden
+    g = SensorGeometry(64, 64)
+    picks = [(w, b) for w, b in windows if b.geometry.width == 64 and b.geometry.height == 64]
+    empty = EventBatch(np.empty(0), np.empty(0), np.empty(0), 0.5, g)
+    batches = [picks[0][1], empty] + [b for _, b in picks[1:]]
+    res, _, _ = sol.solve_windows(batches, evd.SolverParams(), groups=2)
+    assert res[1].status == _lib.EVD_ERR_NO_EVENTS
+    live = [r for j, r in enumerate(res) if j != 1]
+    for r, (w, _) in zip(live, picks):
+        assert r.status == 0 and _same(r, w["result"])
+
+
+def test_iteration_limit_per_window(bnb_golden):
+    meta, windows = bnb_golden
+    lim = meta["iteration_limit"]
+    b = windows[lim["window"]][1]
+    res, _, _ = sol.solve_windows([b, b], evd.SolverParams(max_iterations=lim["max_iterations"]),
+                                  groups=2)
+    for r in res:
+        assert r.status == _lib.EVD_ERR_ITER_LIMIT
+        assert (r.nu, r.contrast, int(r.iterations)) == (f64(lim["nu"]), f64(lim["contrast"]),
+                                                         lim["iterations"])
+
+
+def test_stream_driver_matches_per_window():
+    batches = [synth.sequence_window(k) for k in (10, 11, 12, 13)]
+    samples = evd.estimate_stream_divergence(batches, evd.SolverParams())
+    for s, b in zip(samples, batches):
+        r = evd.maximise_contrast_bnb(b, evd.SolverParams())
+        assert (s.contrast, s.iterations) == (r.contrast, r.iterations)
+        assert s.divergence == evd.divergence_from_velocity(r.nu, b.tau)
