@@ -78,6 +78,9 @@ struct evd_ctx {
     DevBuf<double> segs, fargs;
     DevBuf<unsigned int> fimg;          // batched-frontier images (kept zeroed)
     DevBuf<unsigned long long> facc;
+    DevBuf<unsigned int> pimg;          // batched point images (kept zeroed)
+    DevBuf<double> pargs;
+    DevBuf<unsigned long long> pacc;
     DevBuf<unsigned int> seg_counts;
     TreePlan tree;
     // bound assembly table pow(f/M, 2)
@@ -405,6 +408,9 @@ void evd_destroy(evd_ctx *ctx)
     ctx->fargs.release();
     ctx->fimg.release();
     ctx->facc.release();
+    ctx->pimg.release();
+    ctx->pargs.release();
+    ctx->pacc.release();
     ctx->img.release();
     ctx->simg.release();
     ctx->seg_counts.release();
@@ -523,12 +529,66 @@ int evd_warp_scale(evd_ctx *ctx, const double *t, int64_t n, double nu, double t
     return EVD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+static int point_images_batched(evd_ctx *ctx, const double *nu, int32_t k, int64_t *in_image,
+                                double *contrast)
+{
+    int rc;
+    const long long M = (long long)ctx->W * ctx->H;
+    std::vector<double> host(2 * (size_t)k);
+    for (int j = 0; j < k; j++) {
+        host[j] = nu[j];
+        if ((rc = check_den(ctx, nu[j], ctx->tau, &host[(size_t)k + j]))) return rc;
+    }
+    if ((rc = ensure_tree(ctx, M, ctx->sms))) return rc;
+    // images of up to kb velocities at a time (the contrast pass leaves them zeroed)
+    long long kb = std::max<long long>(32, (4ll << 30) / (M * 4)) / 32 * 32;
+    kb = std::min<long long>(kb, (k + 31) / 32 * 32);
+    if ((long long)ctx->pimg.cap < kb * M) {
+        CU(ctx->pimg.ensure((size_t)(kb * M)));
+        CU(cudaMemsetAsync(ctx->pimg.p, 0, ctx->pimg.cap * sizeof(unsigned int), ctx->stream));
+    }
+    CU(ctx->pargs.ensure(2 * (size_t)k + (size_t)kb * ctx->tree.dev.C + k));
+    CU(ctx->pacc.ensure((size_t)k));
+    CU(cudaMemcpyAsync(ctx->pargs.p, host.data(), host.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemsetAsync(ctx->pacc.p, 0, (size_t)k * sizeof(unsigned long long), ctx->stream));
+    double *d_nu = ctx->pargs.p, *d_den = d_nu + k, *d_out = d_den + k, *d_cut = d_out + k;
+    for (long long j0 = 0; j0 < k; j0 += kb) {
+        const int kk = (int)std::min<long long>(kb, k - j0);
+        launch_points_multi(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, d_nu + j0, d_den + j0, kk,
+                            ctx->W / 2.0, ctx->H / 2.0, ctx->W, ctx->H, ctx->pimg.p, M,
+                            ctx->pacc.p + j0, ctx->tree.dev, d_cut, d_out + j0, ctx->stream);
+        LAUNCHED(3);
+    }
+    std::vector<unsigned long long> ins((size_t)k);
+    CU(cudaMemcpyAsync(ins.data(), ctx->pacc.p, k * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    if (contrast)
+        CU(cudaMemcpyAsync(contrast, d_out, k * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (in_image)
+        for (int j = 0; j < k; j++) in_image[j] = (int64_t)ins[j];
+    return EVD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int evd_point_images(evd_ctx *ctx, const double *nu, int32_t k, int64_t *in_image,
                      double *contrast, uint32_t *counts)
 {
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     int rc = need_events(ctx);
     if (rc) return rc;
+    if (k <= 0) return EVD_OK;
+    CU(cudaSetDevice(ctx->device));
+    if (!counts && k > 1) return point_images_batched(ctx, nu, k, in_image, contrast);
     const long long M = (long long)ctx->W * ctx->H;
     CU(cudaSetDevice(ctx->device));
     CU(ctx->img.ensure(3 * M));

@@ -124,6 +124,11 @@ void launch_image_sums(const unsigned int *img, long long m, unsigned long long 
                        cudaStream_t s);
 void launch_contrast_u32(const unsigned int *img, const unsigned long long *in_image,
                          const TreeDev &tree, double *out, cudaStream_t s);
+void launch_points_multi(const double *xc, const double *yc, const double *t, long long n,
+                         const double *nus, const double *dens, int K, double cx, double cy,
+                         int W, int H, unsigned int *images, long long M,
+                         unsigned long long *in_out, const TreeDev &tree, double *cutvals,
+                         double *contrast, cudaStream_t s);
 void launch_contrast_f64(const double *img, double mu, const TreeDev &tree, double *out,
                          cudaStream_t s);
 void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, unsigned int *counts,

@@ -391,6 +391,71 @@ __global__ void k_contrast_cuts_u32(const unsigned int *img, const unsigned long
     if (threadIdx.x == 0) T.cutval[blockIdx.x] = r;
 }
 
+// ---------------------------------------------------------------- batched points
+// accumulate_image + image_contrast (contrast.py:48-64) at K velocities in one
+// pass: lane j of a warp bins every event at velocity k0 + j (a broadcast load
+// of the event), blocks ordered group-major like k_frontier.  The contrast of
+// every image then follows from one cut-block per (image, cut) and one top
+// block per image; the images are left zeroed.
+__global__ void __launch_bounds__(kThreads) k_points_multi(
+    const double *__restrict__ xc, const double *__restrict__ yc, const double *__restrict__ t,
+    long long n, const double *__restrict__ nus, const double *__restrict__ dens, int K, double cx,
+    double cy, int W, int H, unsigned int *images, long long M, int bpg,
+    unsigned long long *in_out)
+{
+    __shared__ unsigned long long s_in[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int g = blockIdx.x / bpg, tb = blockIdx.x % bpg;
+    const int k = g * 32 + lane;
+    const bool valid = k < K;
+    const int kc = valid ? k : K - 1;
+    const double nu = __ldg(nus + kc), den = __ldg(dens + kc);
+    unsigned int *img = images + (long long)kc * M;
+    if (threadIdx.x < 32) s_in[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long inside = 0;
+    const long long gw = (long long)tb * wpb + warp, nw = (long long)bpg * wpb;
+    for (long long e = gw; e < n; e += nw) {
+        const Warped w = warp_event(__ldg(xc + e), __ldg(yc + e), __ldg(t + e), nu, den, cx, cy);
+        const long long p = floor_bin(w.x, w.y, W, H);
+        if (valid && p >= 0) {
+            atomicAdd(img + p, 1u);
+            inside++;
+        }
+    }
+    if (valid && inside) atomicAdd(s_in + lane, inside);
+    __syncthreads();
+    if (threadIdx.x < 32 && g * 32 + (int)threadIdx.x < K && s_in[threadIdx.x])
+        atomicAdd(in_out + g * 32 + threadIdx.x, s_in[threadIdx.x]);
+}
+
+__global__ void k_contrast_cuts_multi(unsigned int *images, const unsigned long long *in_image,
+                                      TreeDev T, double *cutvals)
+{
+    __shared__ double loc[kCutSmem];
+    const int k = blockIdx.x / T.C, c = blockIdx.x % T.C;
+    const double mu = ddiv((double)in_image[k], (double)T.M);
+    const double r = eval_cut(T, c, SqU32Clear{{images + (long long)k * T.M, mu}}, loc,
+                              SolveArgs{}, 0);
+    if (threadIdx.x == 0) cutvals[(long long)k * T.C + c] = r;
+}
+
+__global__ void k_contrast_top_multi(TreeDev T, const double *cutvals, double *out)
+{
+    __shared__ double v[kCutSmem];
+    const int k = blockIdx.x;
+    for (int i = threadIdx.x; i < T.C; i += blockDim.x) v[i] = cutvals[(long long)k * T.C + i];
+    __syncthreads();
+    for (int h = 0; h < T.top_levels; h++) {
+        for (int j = T.top_lvl[h] + threadIdx.x; j < T.top_lvl[h + 1]; j += blockDim.x) {
+            const int4 tr = T.top[j];
+            v[tr.x] = dadd(v[tr.y], v[tr.z]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = ddiv(dadd(0.0, v[T.top_root]), (double)T.M);
+}
+
 __global__ void k_contrast_cuts_f64(const double *img, double mu, TreeDev T)
 {
     __shared__ double loc[kCutSmem];
@@ -1000,6 +1065,24 @@ void launch_contrast_u32(const unsigned int *img, const unsigned long long *in_i
 {
     k_contrast_cuts_u32<<<tree.C, kThreads, 0, s>>>(img, in_image, tree);
     k_contrast_top<<<1, kThreads, 0, s>>>(tree, out);
+}
+
+void launch_points_multi(const double *xc, const double *yc, const double *t, long long n,
+                         const double *nus, const double *dens, int K, double cx, double cy,
+                         int W, int H, unsigned int *images, long long M,
+                         unsigned long long *in_out, const TreeDev &tree, double *cutvals,
+                         double *contrast, cudaStream_t s)
+{
+    const int groups = (K + 31) / 32;
+    long long bpg = (n + kThreads - 1) / kThreads;
+    if (bpg > (long long)num_sms() * 4) bpg = (long long)num_sms() * 4;
+    if (bpg < 1) bpg = 1;
+    k_points_multi<<<(unsigned)(groups * bpg), kThreads, 0, s>>>(xc, yc, t, n, nus, dens, K, cx,
+                                                                 cy, W, H, images, M, (int)bpg,
+                                                                 in_out);
+    k_contrast_cuts_multi<<<(unsigned)((long long)K * tree.C), kThreads, 0, s>>>(images, in_out,
+                                                                               tree, cutvals);
+    k_contrast_top_multi<<<K, kThreads, 0, s>>>(tree, cutvals, contrast);
 }
 
 void launch_contrast_f64(const double *img, double mu, const TreeDev &tree, double *out,

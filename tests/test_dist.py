@@ -1,0 +1,117 @@
+"""Multi-process host logic of the multi-GPU paths, world_size 2 over gloo (CPU).
+
+The device evaluators are replaced by the pinned CPU oracle, so these tests
+check the sharding, the all-gathers and the replicated batched BnB state.
+"""
+
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import GOLDEN, ROOT, f64
+from oracle import oracle as orc
+from paper_2209_13168_b200 import dist as pdist
+from paper_2209_13168_b200.geometry import DivergenceSample, divergence_from_velocity
+from paper_2209_13168_b200.solver import SolverParams
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_evaluators(batch):
+    def contrasts(nus):
+        return np.array([orc.contrast_at(batch, float(nu)) for nu in nus])
+
+    def bounds(lo, hi):
+        return np.array([orc.bound_terms(batch, float(a), float(b))[2] for a, b in zip(lo, hi)])
+
+    return contrasts, bounds
+
+
+def _oracle_stream(batches, params):
+    out = []
+    for b in batches:
+        if b.n == 0:
+            continue
+        r = orc.maximise_contrast_bnb(b)
+        out.append(DivergenceSample(b.t_end, divergence_from_velocity(r.nu, b.tau), r.contrast,
+                                    r.bound_gap, r.iterations, 0.0))
+    return out
+
+
+def _windows():
+    from paper_2209_13168_b200 import synth
+    d = synth.Descent(64, 64, 300, nu=-0.4, duration=2.0, seed=11)
+    return synth.stream_windows(synth.landing_stream(d), 0.5)
+
+
+def _worker(rank, world, port, queue):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        params = SolverParams()
+        wins = _windows()
+        samples = pdist.estimate_stream_divergence_dist(wins, params, solve_local=_oracle_stream)
+        b = wins[1]
+        c, bd = _oracle_evaluators(b)
+        res = pdist.solve_batched(b, params, k=8, contrasts=c, bounds=bd, split=True)
+        queue.put((rank, [(s.t, s.contrast, s.iterations) for s in samples],
+                   (res.nu, res.contrast, res.rounds, res.nodes)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_bounds_balanced_and_contiguous():
+    sizes = [10, 0, 30, 30, 5, 5, 100, 20]
+    for world in (1, 2, 3, 8):
+        b = pdist.shard_bounds(sizes, world)
+        assert b[0][0] == 0 and b[-1][1] == len(sizes)
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+    two = pdist.shard_bounds(sizes, 2)
+    assert two == [(0, 6), (6, 8)]
+
+
+def test_world2_gloo_windows_and_split_frontier():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort()
+    (_, s0, r0), (_, s1, r1) = outs
+    # both ranks hold the full, identical sample list and the identical BnB state
+    assert s0 == s1 and r0 == r1
+    serial = _oracle_stream(_windows(), SolverParams())
+    assert s0 == [(s.t, s.contrast, s.iterations) for s in serial]
+    # the split batched solve equals the single-process batched solve ...
+    b = _windows()[1]
+    c, bd = _oracle_evaluators(b)
+    one = pdist.solve_batched(b, SolverParams(), k=8, contrasts=c, bounds=bd)
+    assert (one.nu, one.contrast, one.rounds, one.nodes) == r0
+    # ... and is certified within gamma of the reference-order optimum (P3)
+    ref = orc.maximise_contrast_bnb(b)
+    assert one.contrast >= ref.contrast - 0.025
+    assert one.rounds <= ref.iterations
+
+
+def test_batched_matches_reference_within_gamma_on_goldens(bnb_golden):
+    meta, windows = bnb_golden
+    for w, b in windows[:6]:
+        c, bd = _oracle_evaluators(b)
+        res = pdist.solve_batched(b, SolverParams(), k=16, contrasts=c, bounds=bd)
+        ref_c = f64(w["result"]["contrast"])
+        assert res.contrast >= ref_c - 0.025
+        assert res.bound_gap <= 0.025 + 1e-12
