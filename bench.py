@@ -145,6 +145,43 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def frontier_line(ctx, stream):
+    """Config 3: the 4096-leaf frontier of a 999,557-event 640x480 window in one
+    evd_eval_frontier call (device time, best of 3)."""
+    import torch
+    from paper_2209_13168_b200 import contrast as con, frontier as fr, synth
+    from paper_2209_13168_b200.geometry import velocity_domain
+    b = synth.config_window(3)
+    lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
+    con.load_window(b, ctx)
+    con.frontier_terms(b, lo, hi, ctx=ctx, loaded=True)
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, _, mk = con.frontier_terms(b, lo, hi, ctx=ctx, loaded=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        best = t if best is None else min(best, t)
+    return {"intervals": int(lo.size), "events": int(b.n), "seconds_per_call": best,
+            "events_x_bound_evals_per_s": b.n * lo.size / best,
+            "marks": int(mk.sum()), "atomics_per_s": float(mk.sum()) / best}
+
+
+def windows_line(ctx):
+    """Config 4: the 2000-window 240x180 landing sequence in one evd_solve_windows
+    launch (device time)."""
+    import paper_2209_13168_b200 as evd
+    from paper_2209_13168_b200 import solver as sol, synth
+    batches = [synth.sequence_window(k) for k in range(2000)]
+    sol.solve_windows(batches[:64], evd.SolverParams(), ctx=ctx)
+    res, dev_s, groups = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
+    return {"windows": len(batches), "events": int(sum(b.n for b in batches)),
+            "device_s": dev_s, "windows_per_s": len(batches) / dev_s, "solver_groups": groups,
+            "all_ok": all(r.status == 0 for r in res)}
+
+
 def run_gpu(args, rank, world, local):
     import torch
     import paper_2209_13168_b200 as evd
@@ -265,6 +302,9 @@ def run_gpu(args, rank, world, local):
                          "note": "latency-bound sequential BnB: one grid-wide node step per "
                                  "iteration; algorithmic bytes = 24 B x events x node evals"},
         }
+        if world == 1 and not args.no_extra:
+            line["frontier_cfg3"] = frontier_line(ctx, stream)
+            line["windows_cfg4"] = windows_line(ctx)
         if world == 1 and not args.no_cpu:
             threads = host_threads()
             dt, r = cpu_solve_sample(batch, threads)
@@ -285,6 +325,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the config-3 frontier and config-4 window lines")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

@@ -121,6 +121,7 @@ typedef struct {
     int64_t max_frontier; /* largest live queue */
     double device_ms;     /* device time of the solve (CUDA events on the ctx stream) */
     uint64_t marks;       /* pixel increments made in all images (atomic work) */
+    uint64_t exact_events;/* event x node evaluations that needed the exact (division) path */
 } evd_solve_result;
 
 /* Whole solve on the device for the resident window (one cooperative
@@ -138,7 +139,7 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
 typedef struct {
     double nu, contrast, bound_gap;
     int64_t iterations, bound_evals, point_evals, max_frontier;
-    uint64_t marks;
+    uint64_t marks, exact_events;
     int32_t status;
     int32_t groups;   /* solver groups the launch used */
 } evd_window_result;
@@ -148,8 +149,9 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
                       double *device_ms);
 
 /* Device timestamps (ns, %globaltimer) of the last solve (first window of
- * group 0): out[0] = start, then 8 slots per node evaluation (see
- * csrc/evd_internal.h TraceSlot).  *n receives the number of valid entries. */
+ * group 0): out[0] = start, then 10 slots per node evaluation (see
+ * csrc/evd_internal.h TraceSlot: 8 timestamps, then the node's segment marks
+ * and exact-path events).  *n receives the number of valid entries. */
 int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n);
 
 /* Per-block timestamps of the first 128 node evaluations of the last

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -757,6 +758,10 @@ namespace {
 
 // Run the device-resident BnB over n_windows windows of the resident events
 // (window w = events [off[w], off[w+1])) with `groups` independent CTA groups.
+// windows at least this large use the filtered event path (measured: a win at
+// ~1M events, a loss at ~200k where register pressure dominates)
+constexpr long long kFilterMinEvents = 500000;
+
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
                        float *ms_out)
@@ -840,6 +845,8 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         a.trace = ctx->trace.p;
         a.trace_iters = kTraceIters;
         a.btrace = ctx->btrace.p;
+        a.filter = (max_n >= kFilterMinEvents) ? 1 : 0;
+        if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
         CU(launch_solve(a, groups * GB, ctx->stream));
         LAUNCHED(1);
@@ -889,6 +896,7 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
     res->point_evals = w.point_evals;
     res->max_frontier = w.max_fr;
     res->marks = w.marks;
+    res->exact_events = w.exact;
     res->device_ms = ms;
     if (w.status == kStatusIterLimit)
         return fail(ctx, EVD_ERR_ITER_LIMIT,
@@ -932,6 +940,7 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
         r.point_evals = out[w].point_evals;
         r.max_frontier = out[w].max_fr;
         r.marks = out[w].marks;
+        r.exact_events = out[w].exact;
         r.status = out[w].status == kStatusOk ? EVD_OK
                    : out[w].status == kStatusIterLimit ? EVD_ERR_ITER_LIMIT
                    : out[w].status == kStatusEmpty ? EVD_ERR_NO_EVENTS : EVD_ERR_CUDA;

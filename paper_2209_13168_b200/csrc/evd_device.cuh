@@ -48,6 +48,75 @@ __device__ __forceinline__ int fully_inside(double ax, double ay, double bx, dou
             0.0 <= bx && bx < W && 0.0 <= by && by < H) ? 1 : 0;
 }
 
+// ---------------------------------------------------------------- filtered path
+// Approximate warp with r = RN(1/denom) (correctly rounded, computed once per
+// velocity): s~ = RN(num * r) is within 3 ulp-relative of the exact
+// RN(num / denom) (r and both products carry <= 2^-53 relative error each), so
+// the approximate coordinate is within (|x'| + |xc s| + cx) * 1e-15 of the
+// exact one.  kSure(v) below is a margin ~100x that bound; a geometry decided
+// with it is the geometry of the exact values.
+__device__ __forceinline__ Warped warp_approx(double xc, double yc, double t, double nu,
+                                             double rden, double cx, double cy)
+{
+    const double s = dmul(dadd(1.0, dmul(nu, t)), rden);
+    return {dadd(cx, dmul(xc, s)), dadd(cy, dmul(yc, s))};
+}
+
+__device__ __forceinline__ double sure_margin(const Warped &p, double cx, double cy)
+{
+    return 1e-13 * (1.0 + fabs(p.x) + fabs(p.y) + cx + cy);
+}
+
+// true if the exact coordinate lies strictly inside (f, f + 1)
+__device__ __forceinline__ bool sure_cell(double v, double m, double &f)
+{
+    f = floor(v);
+    return v - m > f && v + m < f + 1.0;
+}
+
+// Certified outcome of the point binning (contrast.py:52-55) from an
+// approximate position: returns false if uncertain, else sets pix (-1 when
+// the exact point bins outside the frame).
+__device__ __forceinline__ bool sure_point(const Warped &p, double m, int W, int H, long long &pix)
+{
+    double fx, fy;
+    if (!sure_cell(p.x, m, fx) || !sure_cell(p.y, m, fy)) return false;
+    pix = (fx >= 0.0 && fx < W && fy >= 0.0 && fy < H) ? (long long)fy * W + (long long)fx : -1;
+    return true;
+}
+
+// Certified outcome of one segment a -> b (contrast.py:94-203) from
+// approximate endpoints: false if uncertain; else pix (-1: marks nothing)
+// and inside (the fully-inside indicator).  Two certain cases:
+//  * both endpoints strictly inside the same pixel: every sample of the
+//    reference (p(0) = a, p(1) = a + ddx within 2 ulp of b, p(0.5) between)
+//    is strictly inside it, so the reference marks exactly that pixel if it is
+//    in the frame (else the clip rejects the segment), and the segment is
+//    fully inside iff the pixel is in the frame;
+//  * both endpoints strictly beyond the same frame edge (by the approximation
+//    margin plus the reference's own rounding slack, (|a|+|b|) 2^-50): every
+//    sample is then strictly beyond that edge, and a closed pixel square that
+//    contains a point left of x = 0 (right of x = W, ...) is out of the frame.
+__device__ __forceinline__ bool sure_segment(const Warped &a, const Warped &b, double ma,
+                                             double mb, int W, int H, long long &pix, int &inside)
+{
+    const double sx = ma + mb + 1e-12 * (1.0 + fabs(a.x) + fabs(b.x));
+    const double sy = ma + mb + 1e-12 * (1.0 + fabs(a.y) + fabs(b.y));
+    if ((a.x < -sx && b.x < -sx) || (a.x > W + sx && b.x > W + sx) ||
+        (a.y < -sy && b.y < -sy) || (a.y > H + sy && b.y > H + sy)) {
+        pix = -1;
+        inside = 0;
+        return true;
+    }
+    double fax, fay, fbx, fby;
+    if (!sure_cell(a.x, ma, fax) || !sure_cell(a.y, ma, fay) || !sure_cell(b.x, mb, fbx) ||
+        !sure_cell(b.y, mb, fby) || fax != fbx || fay != fby)
+        return false;
+    inside = (fax >= 0.0 && fax < W && fay >= 0.0 && fay < H) ? 1 : 0;
+    pix = inside ? (long long)fay * W + (long long)fax : -1;
+    return true;
+}
+
 // ---------------------------------------------------------------- supercover
 // Per-event dedup.  The reference marks each pixel at most once per event with
 // a stamp grid (contrast.py:89-91).  The device compares against the previous
@@ -75,19 +144,20 @@ template <class Sink>
 __device__ __forceinline__ int mark_point(double px, double py, int W, int H, Prev &prev,
                                           Sink &sink)
 {
-    // the (up to) 2 x 2 candidate pixels, branch-free so lanes do not diverge
+    // the (up to) 2 x 2 candidate pixels as four predicates built from row /
+    // column tests shared between them, so lanes do not diverge
     const Prev r = point_range(px, py);
+    const bool sx = r.x1 != r.x0, sy = r.y1 != r.y0;
+    const bool px0 = r.x0 >= prev.x0 && r.x0 <= prev.x1, px1 = r.x1 >= prev.x0 && r.x1 <= prev.x1;
+    const bool py0 = r.y0 >= prev.y0 && r.y0 <= prev.y1, py1 = r.y1 >= prev.y0 && r.y1 <= prev.y1;
+    const bool fx0 = (unsigned)r.x0 < (unsigned)W, fx1 = sx && (unsigned)r.x1 < (unsigned)W;
+    const bool fy0 = (unsigned)r.y0 < (unsigned)H, fy1 = sy && (unsigned)r.y1 < (unsigned)H;
+    const int base = r.y0 * W + r.x0;  // the frame has < 2^31 pixels
     int marks = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int ix = (k & 1) ? r.x1 : r.x0, iy = (k & 2) ? r.y1 : r.y0;
-        const bool dup = ((k & 1) && r.x1 == r.x0) || ((k & 2) && r.y1 == r.y0);
-        const bool seen = ix >= prev.x0 && ix <= prev.x1 && iy >= prev.y0 && iy <= prev.y1;
-        if (!dup && !seen && ix >= 0 && ix < W && iy >= 0 && iy < H) {
-            sink(iy * (long long)W + ix);
-            marks++;
-        }
-    }
+    if (fx0 && fy0 && !(px0 && py0)) { sink(base); marks++; }
+    if (fx1 && fy0 && !(px1 && py0)) { sink(base + 1); marks++; }
+    if (fx0 && fy1 && !(px0 && py1)) { sink(base + W); marks++; }
+    if (fx1 && fy1 && !(px1 && py1)) { sink(base + W + 1); marks++; }
     prev = r;
     return marks;
 }
@@ -319,8 +389,13 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
 // its lookahead and refills it with one division on selected operands, so
 // lanes stay converged), mark the midpoint.  Returns false once the chunk is
 // finished.
+#ifdef EVD_OUTLINE_STEP
+#define EVD_STEP_INLINE __noinline__
+#else
+#define EVD_STEP_INLINE __forceinline__
+#endif
 template <class Sink>
-__device__ __forceinline__ bool cursor_step(const SegDesc &d, Cursor &c, int W, int H, Sink &sink,
+__device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, int H, Sink &sink,
                                             int &marks)
 {
     const double cx0 = d.X.c0, ddx = d.X.dd, cy0 = d.Y.c0, ddy = d.Y.dd;

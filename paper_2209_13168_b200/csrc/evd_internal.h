@@ -42,7 +42,7 @@ struct SolveState {
     int mode, done;
     // per-node accumulators, double-buffered by node parity: 0 in_image,
     // 1 fully_inside A, 2 fully_inside B, 3 segment marks, 4 S_bar A, 5 S_bar B,
-    // 7 event work counter
+    // 6 exact-path events, 7 event work counter
     unsigned long long acc[2][8];
     // incumbent and diagnostics
     double nu_hat, c_hat, bound_gap;
@@ -56,7 +56,7 @@ enum WindowStatus : int { kStatusEmpty = 3 };
 struct WindowResult {
     double nu, contrast, bound_gap;
     long long iterations, bound_evals, point_evals, max_fr;
-    unsigned long long marks;
+    unsigned long long marks, exact;
     int status, pad;
 };
 
@@ -81,6 +81,7 @@ struct SolveArgs {
     long long *trace;             // [1 + kTraceSlots*trace_iters] globaltimer ns (group 0, window 0)
     long long trace_iters;
     long long *btrace;            // [kBTraceIters][group_blocks][kBTraceSlots] (or null)
+    int filter;                   // use the filtered (approximate-then-exact) event path
 };
 
 constexpr int kBTraceIters = 128;
@@ -88,7 +89,7 @@ constexpr int kBTraceSlots = 16;
 constexpr int kBTraceMaxBlocks = 2048;
 
 constexpr long long kTraceIters = 1 << 14;
-constexpr int kTraceSlots = 8;
+constexpr int kTraceSlots = 10;
 // per node evaluation: when ...
 enum TraceSlot : int {
     kTrB0Top = 0,      // block 0 starts the node
@@ -99,6 +100,8 @@ enum TraceSlot : int {
     kTrPixelsMax = 5,  // the latest block finished its pixels (atomicMax)
     kTrB0Step0 = 6,    // block 0 left barrier 2
     kTrB0Step1 = 7,    // block 0 finished the BnB step
+    kTrMarks = 8,      // segment-image marks of the node's children (a count, not a time)
+    kTrExact = 9,      // events that took the exact path (a count)
 };
 
 // ---- kernel launchers (evd_kernels.cu); all asynchronous on `s` ----

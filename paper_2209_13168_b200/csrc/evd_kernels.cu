@@ -20,6 +20,7 @@ constexpr int kThreads = 256;
 constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 constexpr int kChunk = 32;            // sample items per supercover chunk
 constexpr int kInlineCrossings = 6;   // shorter segments are sampled by their own lane
+constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -48,6 +49,7 @@ struct AtomicSink {
 
 // Per-warp queue of built segments: lane l owns slots 2l, 2l+1.
 struct WarpQueue {
+    long long ev[64];       // uncertain events awaiting the exact path
     SegDesc d[64];
     unsigned int *img[64];  // image each queued segment marks
     int off[33];  // exclusive prefix of chunk counts per lane
@@ -57,9 +59,9 @@ struct WarpQueue {
 // Build one segment; sample it in the lane when it has at most one crossing,
 // otherwise queue it in the lane's shared-memory slot for warp_drain.
 // Returns the number of queued chunks.
-__device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
-                                                int H, WarpQueue &q, int slot, AtomicSink &sink,
-                                                int &marks)
+__device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double bx, double by,
+                                                    int W, int H, WarpQueue &q, int slot,
+                                                    AtomicSink &sink, int &marks)
 {
     SegDesc d;
     const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
@@ -73,10 +75,19 @@ __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx,
     return c;
 }
 
+// Out-of-line copy for the solve kernel, whose event loop calls it for both
+// child segments: one copy keeps the hot loop inside the instruction cache.
+__device__ __noinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
+                                             int H, WarpQueue &q, int slot, AtomicSink &sink,
+                                             int &marks)
+{
+    return segment_or_queue_inl(ax, ay, bx, by, W, H, q, slot, sink, marks);
+}
+
 // Sample every chunk the warp queued, in rounds of 32: all lanes position
 // their cursors together, then step one item per iteration; chunks hold
 // nearly equal item counts, so the lanes stay converged.
-__device__ __forceinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H)
+__device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H)
 {
     const int lane = threadIdx.x & 31;
     int incl = cA + cB;
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
         int c = 0, m = 0;
         if (valid) {
             fi += fully_inside(a.x, a.y, b.x, b.y, W, H);
-            c = segment_or_queue(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
+            c = segment_or_queue_inl(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
         }
         if (__any_sync(0xffffffffu, c != 0)) warp_drain(wq, c, 0, W, H);
     }
@@ -558,10 +569,12 @@ __device__ __forceinline__ FrontierEntry entry_load(const FrontierEntry *src)
 // BnB control state, identical in every block.
 struct Replica {
     double lo, hi, c, den_lo, den_c, den_hi;  // node under evaluation
+    double r_lo, r_c, r_hi;                   // RN(1 / den) for the filtered path
     int mode, done, status, parity;
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
     unsigned long long marks;  // pixel increments of all images over the solve
+    unsigned long long exact;  // events that took the exact (uncertain) path
     // this node's integer accumulators and pow(fi/M, 2) table values
     unsigned long long fiA, fiB, sA, sB;
     double p2A, p2B;
@@ -693,6 +706,9 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
             R.den_lo = dadd(1.0, dmul(top.lo, a.tau));
             R.den_c = dadd(1.0, dmul(c, a.tau));
             R.den_hi = dadd(1.0, dmul(top.hi, a.tau));
+            R.r_lo = ddiv(1.0, R.den_lo);
+            R.r_c = ddiv(1.0, R.den_c);
+            R.r_hi = ddiv(1.0, R.den_hi);
             R.mode = kModeNode;
         }
     }
@@ -786,6 +802,7 @@ constexpr size_t kStepBytes = kCutSmem * sizeof(double) + kFrView * sizeof(Front
 constexpr size_t kRegionA = kQueueBytes > kStepBytes ? kQueueBytes : kStepBytes;
 constexpr size_t kSolveSmemBytes = kRegionA + sizeof(TreeCache);
 
+template <bool FILTER>
 __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -838,6 +855,9 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             R.den_lo = a.den_lo0;
             R.den_c = a.den_c0;
             R.den_hi = a.den_hi0;
+            R.r_lo = ddiv(1.0, R.den_lo);
+            R.r_c = ddiv(1.0, R.den_c);
+            R.r_hi = ddiv(1.0, R.den_hi);
             R.mode = kModeRoot;
             R.done = 0;
             R.status = kStatusOk;
@@ -847,6 +867,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             R.bound_gap = 0.0;
             R.iterations = R.bound_evals = R.point_evals = R.next_counter = R.fr_n = R.max_fr = 0;
             R.marks = 0;
+            R.exact = 0;
             R.n_pending = 0;
             R.n_pushed = 0;
         }
@@ -855,6 +876,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             const int mode = R.mode, par = R.parity;
             const double lo = R.lo, hi = R.hi, c = R.c;
             const double den_lo = R.den_lo, den_c = R.den_c, den_hi = R.den_hi;
+            const double r_lo = R.r_lo, r_c = R.r_c, r_hi = R.r_hi;
             const long long it = R.iterations;
             unsigned long long *acc = st->acc[par];
             const bool tr = tracer && w == 0;
@@ -866,44 +888,138 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             // the root); short segments in the lane, long ones spread over the
             // warp.  First round static, then warps take batches of 32 events
             // from the node's work counter (acc[7]) so CTAs finish together.
-            unsigned long long v[4] = {0, 0, 0, 0};
+            unsigned long long v[4] = {0, 0, 0, 0};  // in_image, fi A, fi B, marks
+            unsigned long long vex[1] = {0};           // events on the exact path
             AtomicSink sa{A}, sb{B};
-            long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
-            while (base < n) {
-                const long long i = base + lane;
-                int cA = 0, cB = 0, dummy = 0;
-                if (i < n) {
-                    const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
-                    const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
-                    const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
-                    const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
-                    const long long p = floor_bin(wc.x, wc.y, W, H);
-                    if (p >= 0) {
-                        atomicAdd(P + p, 1u);
-                        v[0]++;
+            // the filtered path pays off once segments are short; wide nodes
+            // (and the FILTER=false kernel) go straight to the exact path --
+            // both give the same images
+            if (!FILTER || dsub(hi, lo) > kFilterWidth) {
+                // every event on the exact path, one per lane; first round
+                // static, then batches of 32 from the node's work counter
+                long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
+                while (base < n) {
+                    const long long i = base + lane;
+                    int cA = 0, cB = 0, dummy = 0;
+                    if (i < n) {
+                        const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
+                        const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
+                        const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
+                        const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
+                        const long long p = floor_bin(wc.x, wc.y, W, H);
+                        if (p >= 0) {
+                            atomicAdd(P + p, 1u);
+                            v[0]++;
+                        }
+                        if (mode == kModeRoot) {
+                            v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                            cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa,
+                                                  dummy);
+                        } else {
+                            v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
+                            cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa,
+                                                  dummy);
+                            v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
+                            cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1,
+                                                  sb, dummy);
+                        }
+                        vex[0]++;
                     }
-                    if (mode == kModeRoot) {
-                        v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                        cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
-                    } else {
-                        v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                        cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
-                        v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                        cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb,
-                                              dummy);
-                    }
+                    if (__any_sync(0xffffffffu, (cA | cB) != 0))
+                        dummy += warp_drain(wq, cA, cB, W, H);
+                    v[3] += dummy;
+                    long long nb = 0;
+                    if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+                    base = __shfl_sync(0xffffffffu, nb, 0);
                 }
-                if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain(wq, cA, cB, W, H);
-                v[3] += dummy;
-                long long nb = 0;
-                if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
-                base = __shfl_sync(0xffffffffu, nb, 0);
+            } else {
+                int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
+                long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
+                while (true) {
+                    const bool more = base < n;
+                    int dummy = 0;
+                    if (more) {
+                        // filtered path: certify all three results from approximate
+                        // warps; uncertain events are queued for the exact path
+                        const long long i = base + lane;
+                        bool exact = false;
+                        if (i < n) {
+                            const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
+                            const Warped ql = warp_approx(x, y, t, lo, r_lo, a.cx, a.cy);
+                            const Warped qc = warp_approx(x, y, t, c, r_c, a.cx, a.cy);
+                            const Warped qh = warp_approx(x, y, t, hi, r_hi, a.cx, a.cy);
+                            const double ml = sure_margin(ql, a.cx, a.cy);
+                            const double mc = sure_margin(qc, a.cx, a.cy);
+                            const double mh = sure_margin(qh, a.cx, a.cy);
+                            long long pp, pa, pb = -1;
+                            int ia, ib = 0;
+                            const bool sure = sure_point(qc, mc, W, H, pp) &&
+                                              (mode == kModeRoot
+                                                   ? sure_segment(ql, qh, ml, mh, W, H, pa, ia)
+                                                   : (sure_segment(ql, qc, ml, mc, W, H, pa, ia) &&
+                                                      sure_segment(qc, qh, mc, mh, W, H, pb, ib)));
+                            if (sure) {
+                                if (pp >= 0) { atomicAdd(P + pp, 1u); v[0]++; }
+                                if (pa >= 0) { atomicAdd(A + pa, 1u); dummy++; }
+                                if (pb >= 0) { atomicAdd(B + pb, 1u); dummy++; }
+                                v[1] += ia;
+                                v[2] += ib;
+                            } else {
+                                exact = true;
+                            }
+                        }
+                        const unsigned bal = __ballot_sync(0xffffffffu, exact);
+                        if (exact) wq.ev[nq + __popc(bal & ((1u << lane) - 1u))] = i;
+                        nq += __popc(bal);
+                        __syncwarp();
+                        long long nb = 0;
+                        if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+                        base = __shfl_sync(0xffffffffu, nb, 0);
+                    }
+                    if (nq >= 32 || (!more && nq > 0)) {
+                        // exact path for 32 queued events at a time (full lanes)
+                        const int take = nq < 32 ? nq : 32;
+                        const long long i = lane < take ? wq.ev[nq - take + lane] : -1;
+                        nq -= take;
+                        __syncwarp();
+                        int cA = 0, cB = 0;
+                        if (i >= 0) {
+                            vex[0]++;
+                            const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
+                            const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
+                            const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
+                            const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
+                            const long long p = floor_bin(wc.x, wc.y, W, H);
+                            if (p >= 0) {
+                                atomicAdd(P + p, 1u);
+                                v[0]++;
+                            }
+                            if (mode == kModeRoot) {
+                                v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                                cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa,
+                                                      dummy);
+                            } else {
+                                v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
+                                cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa,
+                                                      dummy);
+                                v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
+                                cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1,
+                                                      sb, dummy);
+                            }
+                        }
+                        if (__any_sync(0xffffffffu, (cA | cB) != 0))
+                            dummy += warp_drain(wq, cA, cB, W, H);
+                    }
+                    v[3] += dummy;
+                    if (!more && nq == 0) break;
+                }
             }
             __syncthreads();
             if (tr && gb == 0) trace_point(a, it, kTrB0Events);
             if (tr) trace_max(a, it, kTrEventsMax);
             if (tr) btrace_point(a, it, 1);
             block_add_u64<4>(v, acc);
+            block_add_u64<1>(vex, acc + 6);
             grid_sync(ctr, target, GB);
             if (tr) bclock(a, it, 4);
             if (tr && gb == 0) trace_point(a, it, kTrB0Pixels0);
@@ -958,6 +1074,11 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
                 R.sA = __ldcg(acc + 4);
                 R.sB = __ldcg(acc + 5);
                 R.marks += __ldcg(acc + 0) + __ldcg(acc + 3);
+                R.exact += __ldcg(acc + 6);
+                if (tr && gb == 0 && it < a.trace_iters) {  // per-node work counters
+                    a.trace[1 + kTraceSlots * it + kTrMarks] = (long long)__ldcg(acc + 3);
+                    a.trace[1 + kTraceSlots * it + kTrExact] = (long long)__ldcg(acc + 6);
+                }
             }
             __syncthreads();
             if (tr) bclock(a, it, 10);
@@ -980,6 +1101,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             r.point_evals = R.point_evals;
             r.max_fr = R.max_fr;
             r.marks = R.marks;
+            r.exact = R.exact;
             r.status = R.status;
         }
     }
@@ -997,7 +1119,10 @@ static void set_attrs()
                          (int)kBoundSmem);
     cudaFuncSetAttribute(k_frontier, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBoundSmem);
-    cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem);
+    cudaFuncSetAttribute(k_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSolveSmem);
+    cudaFuncSetAttribute(k_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSolveSmem);
     g_attrs = true;
 }
 
@@ -1105,7 +1230,7 @@ int solve_grid_blocks(int device)
 {
     set_attrs();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kSolveThreads, kSolveSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<true>, kSolveThreads, kSolveSmem);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm < 1) per_sm = 1;
@@ -1117,7 +1242,10 @@ cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s)
     set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
-    return cudaLaunchCooperativeKernel((const void *)k_solve, dim3(blocks), dim3(kSolveThreads),
+    // the filtered path (approximate warps, exact fallback) pays off for large
+    // windows; small ones keep the leaner exact-only event loop
+    const void *fn = a.filter ? (const void *)k_solve<true> : (const void *)k_solve<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kSolveThreads),
                                        params, kSolveSmem, s);
 }
 

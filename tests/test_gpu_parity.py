@@ -144,6 +144,21 @@ def test_bnb_small_windows(bnb_golden):
         assert _same(r, w["result"]), w["result"]
 
 
+@pytest.mark.parametrize("path", ["0", "1"])
+def test_bnb_both_event_paths(bnb_golden, monkeypatch, path):
+    """The solve kernel's exact-only and filtered (approximate warp, exact
+    fallback) event paths, forced on every golden window and config 1/2."""
+    monkeypatch.setenv("EVD_SOLVE_FILTER", path)
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        assert _same(evd.maximise_contrast_bnb(batch, evd.SolverParams()), w["result"])
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        cfgs = json.load(fh)["configs"]
+    for cfg in ("1", "2"):
+        r, st = sol.solve_window(synth.config_window(int(cfg)), evd.SolverParams())
+        assert _same(r, cfgs[cfg]["result"])
+
+
 def test_bnb_trace_nodes(bnb_golden):
     """Every node the reference evaluated: centre contrast and both child c_bar bits."""
     meta, windows = bnb_golden

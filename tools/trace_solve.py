@@ -7,6 +7,9 @@ Per node evaluation (us, from block 0's start of the node):
   px    block 0's pixels      maxpx  the slowest block's pixels
   bar2  last pixels -> block 0 leaves barrier 2
   step  block 0's BnB step    total  node to node
+  Mmarks  segment-image marks of the node (millions)
+  G/s     marks per ns of the event phase (the atomic roofline column)
+  exact%  events on the exact path
 """
 
 import os
@@ -20,7 +23,7 @@ sys.path.insert(0, ROOT)
 import paper_2209_13168_b200 as evd  # noqa: E402
 from paper_2209_13168_b200 import _lib, solver as sol, synth  # noqa: E402
 
-SLOTS = 8
+SLOTS = 10
 
 
 def trace(ctx):
@@ -41,7 +44,8 @@ def main():
         r, st = sol.solve_window(b, evd.SolverParams())
     tr = trace(_lib.context())
     k = (len(tr) - 1) // SLOTS
-    T = tr[1:1 + SLOTS * k].reshape(k, SLOTS).astype(np.float64) / 1e3
+    raw = tr[1:1 + SLOTS * k].reshape(k, SLOTS)
+    T = raw[:, :8].astype(np.float64) / 1e3
     k = min(k, st.point_evals)
     cols = {
         "b0ev": T[:k, 1] - T[:k, 0],
@@ -52,8 +56,13 @@ def main():
         "bar2": T[:k, 6] - T[:k, 5],
         "step": T[:k, 7] - T[:k, 6],
         "total": np.r_[T[1:k, 0] - T[:k - 1, 0], np.nan],
+        "Mmarks": raw[:k, 8] / 1e6,
+        "G/s": raw[:k, 8] / (T[:k, 2] - T[:k, 0]) / 1e3,  # segment marks / event phase
+        "exact%": 100.0 * raw[:k, 9] / b.n,
     }
-    print(f"cfg {cfg}: n={b.n} iterations={r.iterations} device_ms={st.device_ms:.3f}")
+    res, _ = sol.solve_loaded(_lib.context(), evd.SolverParams())
+    print(f"cfg {cfg}: n={b.n} iterations={r.iterations} device_ms={st.device_ms:.3f} "
+          f"exact-path share={res.exact_events / (b.n * res.point_evals):.3f}")
     print("node " + " ".join(f"{c:>8s}" for c in cols))
     show = range(k) if "--all" in sys.argv else list(range(min(k, 12))) + list(range(max(12, k - 6), k))
     for i in show:
