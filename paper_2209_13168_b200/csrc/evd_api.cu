@@ -919,11 +919,14 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
         return fail(ctx, EVD_ERR_ARG, "window offsets outside the resident events");
     for (int w = 0; w < n_windows; w++)
         if (offsets[w + 1] < offsets[w]) return fail(ctx, EVD_ERR_ARG, "offsets must be non-decreasing");
-    if (groups <= 0) {  // auto: ~2 events per thread per group, at least one window per group
+    if (groups <= 0) {
+        // auto: ~20 events per thread per group, at least one window per group
+        // (cfg4, 2000 windows of ~20k events: 74 groups of 2 CTAs measured best;
+        // smaller groups trade the grid barrier for per-thread event loops)
         long long tot = offsets[n_windows] - offsets[0];
         const double avg = (double)tot / n_windows;
         if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
-        const int per = std::max(1, (int)std::ceil(avg / (2.0 * solve_block_threads())));
+        const int per = std::max(1, (int)std::ceil(avg / (20.0 * solve_block_threads())));
         groups = std::max(1, std::min(n_windows, ctx->solve_blocks / per));
     }
     std::vector<WindowResult> out;

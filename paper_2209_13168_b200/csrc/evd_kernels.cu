@@ -18,8 +18,10 @@ constexpr int kThreads = 256;
 #define EVD_SOLVE_MINB 1
 #endif
 constexpr int kSolveThreads = EVD_SOLVE_THREADS;
-constexpr int kChunk = 32;            // sample items per supercover chunk
-constexpr int kInlineCrossings = 6;   // shorter segments are sampled by their own lane
+#ifndef EVD_CHUNK
+#define EVD_CHUNK 32
+#endif
+constexpr int kChunk = EVD_CHUNK;  // sample items per supercover chunk
 constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
 
 static int g_num_sms = 0;
@@ -56,9 +58,15 @@ struct WarpQueue {
     int na[32];   // chunks of the lane's first segment
 };
 
-// Build one segment; sample it in the lane when it has at most one crossing,
-// otherwise queue it in the lane's shared-memory slot for warp_drain.
-// Returns the number of queued chunks.
+// Build one segment and queue it in the lane's shared-memory slot for
+// warp_drain (single-pixel and off-frame segments finish in build_segment);
+// segments with at most INLINE crossings are sampled by their own lane.
+// Returns the number of queued chunks.  The solve kernel queues everything
+// (INLINE = -1): its lanes hold unrelated events, so in-lane sampling diverges,
+// and the extra sampler copy costs registers and I-cache (measured slower).
+// The frontier kernel's lanes hold one event at neighbouring intervals --
+// segments of nearly equal length -- and keeps short ones in the lane.
+template <int INLINE>
 __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double bx, double by,
                                                     int W, int H, WarpQueue &q, int slot,
                                                     AtomicSink &sink, int &marks)
@@ -66,7 +74,7 @@ __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double
     SegDesc d;
     const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
     if (c == 0) return 0;
-    if (d.X.n + d.Y.n <= kInlineCrossings) {
+    if (INLINE >= 0 && d.X.n + d.Y.n <= INLINE) {
         marks += sample_chunk(d, 0, W, H, sink);
         return 0;
     }
@@ -81,7 +89,7 @@ __device__ __noinline__ int segment_or_queue(double ax, double ay, double bx, do
                                              int H, WarpQueue &q, int slot, AtomicSink &sink,
                                              int &marks)
 {
-    return segment_or_queue_inl(ax, ay, bx, by, W, H, q, slot, sink, marks);
+    return segment_or_queue_inl<-1>(ax, ay, bx, by, W, H, q, slot, sink, marks);
 }
 
 // Sample every chunk the warp queued, in rounds of 32: all lanes position
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
         int c = 0, m = 0;
         if (valid) {
             fi += fully_inside(a.x, a.y, b.x, b.y, W, H);
-            c = segment_or_queue_inl(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
+            c = segment_or_queue_inl<6>(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
         }
         if (__any_sync(0xffffffffu, c != 0)) warp_drain(wq, c, 0, W, H);
     }

@@ -19,7 +19,7 @@ def _same(r, ref):
         f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
 
 
-@pytest.mark.parametrize("groups", [0, 1, 3, 7])
+@pytest.mark.parametrize("groups", [0, 1, 3, 7, 74, 148])
 def test_sequence_windows_match_reference(groups):
     with open(os.path.join(GOLDEN, "bnb.json")) as fh:
         seq = json.load(fh)["sequence"]
