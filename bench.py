@@ -196,7 +196,11 @@ def run_gpu(args, rank, world, local):
     batch = synth.config_window(2)
     params = evd.SolverParams()
     ctx = _lib.context(local)
-    stream = torch.cuda.current_stream()
+    # one explicit stream for the library, the flush and the timing events
+    # (torch's default stream has handle 0, which evd_set_stream reads as
+    # "the context's own stream")
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.lib.evd_set_stream(ctx.h, _lib._vp(stream.cuda_stream))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 

@@ -148,7 +148,9 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
                       const evd_solve_params *params, evd_window_result *results,
                       double *device_ms);
 
-/* Device timestamps (ns, %globaltimer) of the last solve (first window of
+/* Tracing is off unless the environment holds EVD_TRACE=1 when the context
+ * is created (it costs a few percent).
+ * Device timestamps (ns, %globaltimer) of the last solve (first window of
  * group 0): out[0] = start, then 10 slots per node evaluation (see
  * csrc/evd_internal.h TraceSlot: 8 timestamps, then the node's segment marks
  * and exact-path events).  *n receives the number of valid entries. */

@@ -96,6 +96,7 @@ struct evd_ctx {
     DevBuf<WindowResult> wres;
     DevBuf<long long> trace, btrace;
     long long trace_n = 0;
+    bool trace_on = false;  // EVD_TRACE=1 at evd_create: record solve timelines
     int solve_blocks = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
@@ -386,6 +387,7 @@ int evd_create(int device, evd_ctx **out)
         return fail(nullptr, EVD_ERR_ARG, "device %d out of range (%d devices)", device, count);
     ctx = new evd_ctx();
     ctx->device = device;
+    if (const char *t = getenv("EVD_TRACE")) ctx->trace_on = t[0] == '1';
     CU(cudaSetDevice(device));
     CU(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
     CU(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
@@ -793,10 +795,12 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     }
     CU(ctx->state.ensure(groups));
     CU(ctx->bar2.ensure(2 * (size_t)groups));
-    CU(ctx->trace.ensure(1 + kTraceSlots * kTraceIters));
-    CU(ctx->btrace.ensure((size_t)kBTraceIters * kBTraceMaxBlocks * kBTraceSlots));
-    CU(cudaMemsetAsync(ctx->trace.p, 0, (1 + kTraceSlots * kTraceIters) * sizeof(long long),
-                       ctx->stream));
+    if (ctx->trace_on) {
+        CU(ctx->trace.ensure(1 + kTraceSlots * kTraceIters));
+        CU(ctx->btrace.ensure((size_t)kBTraceIters * kBTraceMaxBlocks * kBTraceSlots));
+        CU(cudaMemsetAsync(ctx->trace.p, 0, (1 + kTraceSlots * kTraceIters) * sizeof(long long),
+                           ctx->stream));
+    }
     CU(ctx->woff.ensure(n_windows + 1));
     CU(ctx->wres.ensure(n_windows));
     CU(cudaMemcpyAsync(ctx->woff.p, off, (n_windows + 1) * sizeof(long long),
@@ -842,9 +846,9 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         a.fr_cap = cap;
         a.bar = ctx->bar2.p;
         a.res = ctx->wres.p;
-        a.trace = ctx->trace.p;
+        a.trace = ctx->trace_on ? ctx->trace.p : nullptr;
         a.trace_iters = kTraceIters;
-        a.btrace = ctx->btrace.p;
+        a.btrace = ctx->trace_on ? ctx->btrace.p : nullptr;
         a.filter = (max_n >= kFilterMinEvents) ? 1 : 0;
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -866,7 +870,7 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         if (!again) break;
         cap *= 8;  // frontier outgrew its buffer: rerun (the solve is deterministic)
     }
-    ctx->trace_n = 1 + kTraceSlots * std::min<long long>(out[0].iterations + 1, kTraceIters);
+    ctx->trace_n = !ctx->trace_on ? 0 : 1 + kTraceSlots * std::min<long long>(out[0].iterations + 1, kTraceIters);
     if (ms_out) *ms_out = total_ms;
     return EVD_OK;
 }

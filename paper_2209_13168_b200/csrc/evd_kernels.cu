@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
     const int GB = a.group_blocks;
     const int grp = blockIdx.x / GB, gb = blockIdx.x % GB;
     if (grp >= a.groups) return;
-    const bool tracer = grp == 0;
+    const bool tracer = grp == 0 && a.trace != nullptr;
     unsigned long long *ctr = a.bar + 2 * grp;
     unsigned long long target = 0;
     SolveState *st = a.st + grp;

@@ -24,7 +24,8 @@ def main():
     b = synth.config_window(3)
     lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
     ctx = _lib.context()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # explicit: handle 0 would mean the context's own stream
+    torch.cuda.set_stream(stream)
     ctx.lib.evd_set_stream(ctx.h, _lib._vp(stream.cuda_stream))
     con.load_window(b, ctx)
     for _ in range(2):

@@ -19,6 +19,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+os.environ["EVD_TRACE"] = "1"  # read when the libevd context is created
 
 import paper_2209_13168_b200 as evd  # noqa: E402
 from paper_2209_13168_b200 import _lib, solver as sol, synth  # noqa: E402
