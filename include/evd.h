@@ -161,6 +161,12 @@ int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n);
  * done, step done (diagnostics). */
 int evd_solve_block_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int32_t *blocks);
 
+/* Diagnostics: the solve kernel's exact event pass for one child evaluation
+ * of [lo, hi] (point image at the centre, both child segment images), run
+ * `reps` times in one launch on the solve grid; span_ns[r] = device time of
+ * rep r.  Results are discarded. */
+int evd_probe_events(evd_ctx *ctx, double lo, double hi, int32_t reps, double *span_ns);
+
 /* ---- helpers ----------------------------------------------------------- */
 /* out[f] = pow(f / m, 2.0) through the process's libm pow(), f = 0..n: the
  * value CPython's `mu_lower**2` yields (contrast.py:250-251). */

@@ -26,6 +26,7 @@ SYMBOLS = (
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
     "evd_rasterize_segments",
     "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
+    "evd_probe_events",
     "evd_pow2_table",
 )
 
@@ -93,6 +94,7 @@ _SIGS = {
                                          ctypes.POINTER(WindowResult), _d]),
     "evd_solve_trace": (ctypes.c_int, [_vp, _i64p, _i64, _i64p]),
     "evd_solve_block_trace": (ctypes.c_int, [_vp, _i64p, _i64, ctypes.POINTER(_i32)]),
+    "evd_probe_events": (ctypes.c_int, [_vp, _f64, _f64, _i32, _d]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
 }
 

@@ -95,6 +95,8 @@ struct evd_ctx {
     DevBuf<long long> woff;            // window offsets
     DevBuf<WindowResult> wres;
     DevBuf<long long> trace, btrace;
+    DevBuf<unsigned long long> probe_ctr, probe_span;  // evd_probe_events
+    DevBuf<unsigned int> probe_img;
     long long trace_n = 0;
     bool trace_on = false;  // EVD_TRACE=1 at evd_create: record solve timelines
     int solve_blocks = 0;
@@ -424,6 +426,11 @@ void evd_destroy(evd_ctx *ctx)
     ctx->bar2.release();
     ctx->woff.release();
     ctx->wres.release();
+    ctx->trace.release();
+    ctx->btrace.release();
+    ctx->probe_ctr.release();
+    ctx->probe_span.release();
+    ctx->probe_img.release();
     TreePlan &tp = ctx->tree;
     tp.leaves.release();
     tp.cut_leaf0.release();
@@ -965,6 +972,39 @@ int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n)
     if (k > 0 && ctx->trace.p) {
         CU(cudaMemcpy(out, ctx->trace.p, k * sizeof(long long), cudaMemcpyDeviceToHost));
     }
+    return EVD_OK;
+}
+
+int evd_probe_events(evd_ctx *ctx, double lo, double hi, int32_t reps, double *span_ns)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (reps < 1 || reps > 1024 || !span_ns) return fail(ctx, EVD_ERR_ARG, "bad probe arguments");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    const double nu3[3] = {lo, 0.5 * (lo + hi), hi};
+    double den3[3];
+    for (int k = 0; k < 3; k++)
+        if ((rc = check_den(ctx, nu3[k], ctx->tau, den3 + k))) return rc;
+    if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
+    const long long M = (long long)ctx->W * ctx->H;
+    DevBuf<unsigned long long> &ctrs = ctx->probe_ctr, &span = ctx->probe_span;
+    DevBuf<unsigned int> &scratch = ctx->probe_img;
+    CU(ctrs.ensure(8 * (size_t)reps));
+    CU(span.ensure(2 * (size_t)reps));
+    CU(scratch.ensure(6 * (size_t)M));
+    CU(cudaMemsetAsync(ctrs.p, 0, 8 * reps * sizeof(unsigned long long), ctx->stream));
+    std::vector<unsigned long long> h(2 * (size_t)reps);
+    for (int r = 0; r < reps; r++) { h[2 * r] = ~0ull; h[2 * r + 1] = 0; }
+    CU(cudaMemcpyAsync(span.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemsetAsync(scratch.p, 0, 6 * M * sizeof(unsigned int), ctx->stream));
+    const double cx = ctx->W / 2.0, cy = ctx->H / 2.0;
+    CU(launch_event_probe(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, nu3, den3, cx, cy,
+                          ctx->W, ctx->H, ctx->solve_blocks, reps, ctrs.p, span.p, scratch.p,
+                          ctx->stream));
+    LAUNCHED(1);
+    CU(cudaMemcpyAsync(h.data(), span.p, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < reps; r++) span_ns[r] = (double)(h[2 * r + 1] - h[2 * r]);
     return EVD_OK;
 }
 

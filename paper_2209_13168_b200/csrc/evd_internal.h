@@ -139,5 +139,9 @@ void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, 
 int solve_grid_blocks(int device);
 int solve_block_threads();
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
+cudaError_t launch_event_probe(const double *xc, const double *yc, const double *t, long long n,
+                               const double *nu3, const double *den3, double cx, double cy,
+                               int W, int H, int blocks, int reps, unsigned long long *ctrs,
+                               unsigned long long *span, unsigned int *scratch, cudaStream_t s);
 
 }  // namespace evd

@@ -552,6 +552,97 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     __syncthreads();
 }
 
+// One node's events on the exact path (k_solve's event phase; also timed
+// alone by k_event_probe): every event, three warps (lo, centre, hi); point
+// image at the centre, segment images of both children (root: of the root),
+// segments sampled warp-cooperatively by warp_drain.  First round static, then
+// warps take batches of 32 events from the node's work counter (acc[7]) so
+// CTAs finish together.
+struct EventJob {
+    const double *xc, *yc, *tw;
+    long long n;
+    double lo, c, hi, den_lo, den_c, den_hi, cx, cy;
+    int W, H;
+    unsigned int *P, *A, *B;
+    int mode;
+    unsigned long long *acc;
+    long long gsz;
+    int gb;
+};
+
+__device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &wq,
+                                                 unsigned long long (&v)[4],
+                                                 unsigned long long (&vex)[1])
+{
+    const int lane = threadIdx.x & 31, W = j.W, H = j.H;
+    const double *xc = j.xc, *yc = j.yc, *tw = j.tw;
+    const long long n = j.n, gsz = j.gsz;
+    unsigned int *P = j.P;
+    unsigned long long *acc = j.acc;
+    AtomicSink sa{j.A}, sb{j.B};
+    // One static batch of 32 events per warp, then batches of 32 from the
+    // node's work counter.  The pass is latency-bound (a few batches per warp
+    // at narrow nodes), so claiming several batches at once was measured
+    // slower (tools/probe_events.py): it serialises them on fewer warps.
+    long long base = j.gb * (long long)blockDim.x + (threadIdx.x & ~31);
+    while (base < n) {
+        const long long i = base + lane;
+        int cA = 0, cB = 0, dummy = 0;
+        if (i < n) {
+            const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
+            const Warped wl = warp_event(x, y, t, j.lo, j.den_lo, j.cx, j.cy);
+            const Warped wc = warp_event(x, y, t, j.c, j.den_c, j.cx, j.cy);
+            const Warped wh = warp_event(x, y, t, j.hi, j.den_hi, j.cx, j.cy);
+            const long long p = floor_bin(wc.x, wc.y, W, H);
+            if (p >= 0) {
+                atomicAdd(P + p, 1u);
+                v[0]++;
+            }
+            if (j.mode == kModeRoot) {
+                v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
+            } else {
+                v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
+                cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
+                v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
+                cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb, dummy);
+            }
+            vex[0]++;
+        }
+        if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain(wq, cA, cB, W, H);
+        v[3] += dummy;
+        long long nb = 0;
+        if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+        base = __shfl_sync(0xffffffffu, nb, 0);
+    }
+}
+
+// Diagnostics: the exact event pass of one child-node evaluation, timed alone
+// (reps launches' worth in one kernel, each rep with its own work counter and
+// scratch images; globaltimer span per rep in span[2*r], span[2*r+1]).
+__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB)
+    k_event_probe(EventJob j, int reps, unsigned long long *ctrs, unsigned long long *span,
+                  unsigned int *scratch, long long M)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    for (int r = 0; r < reps; r++) {
+        EventJob jr = j;
+        jr.acc = ctrs + 8 * r;
+        jr.gb = blockIdx.x;
+        jr.P = scratch + (long long)(r % 2) * 3 * M;
+        jr.A = jr.P + M;
+        jr.B = jr.A + M;
+        unsigned long long v[4] = {0, 0, 0, 0}, vex[1] = {0};
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMin(span + 2 * r, (unsigned long long)globaltimer());
+        event_pass_exact(jr, wq, v, vex);
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(span + 2 * r + 1, (unsigned long long)globaltimer());
+        if (v[3] == 0xffffffffffffull) span[0] = 0;  // keep the counts live
+    }
+}
+
 __device__ __forceinline__ bool better(double b1, long long c1, double b2, long long c2)
 {
     // heapq order on (-c_bar, counter): larger bound first, FIFO among ties
@@ -903,43 +994,9 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             // (and the FILTER=false kernel) go straight to the exact path --
             // both give the same images
             if (!FILTER || dsub(hi, lo) > kFilterWidth) {
-                // every event on the exact path, one per lane; first round
-                // static, then batches of 32 from the node's work counter
-                long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
-                while (base < n) {
-                    const long long i = base + lane;
-                    int cA = 0, cB = 0, dummy = 0;
-                    if (i < n) {
-                        const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
-                        const Warped wl = warp_event(x, y, t, lo, den_lo, a.cx, a.cy);
-                        const Warped wc = warp_event(x, y, t, c, den_c, a.cx, a.cy);
-                        const Warped wh = warp_event(x, y, t, hi, den_hi, a.cx, a.cy);
-                        const long long p = floor_bin(wc.x, wc.y, W, H);
-                        if (p >= 0) {
-                            atomicAdd(P + p, 1u);
-                            v[0]++;
-                        }
-                        if (mode == kModeRoot) {
-                            v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                            cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa,
-                                                  dummy);
-                        } else {
-                            v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                            cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa,
-                                                  dummy);
-                            v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                            cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1,
-                                                  sb, dummy);
-                        }
-                        vex[0]++;
-                    }
-                    if (__any_sync(0xffffffffu, (cA | cB) != 0))
-                        dummy += warp_drain(wq, cA, cB, W, H);
-                    v[3] += dummy;
-                    long long nb = 0;
-                    if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
-                    base = __shfl_sync(0xffffffffu, nb, 0);
-                }
+                EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
+                           W, H, P, A, B, mode, acc, gsz, gb};
+                event_pass_exact(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
                 long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
@@ -1131,6 +1188,8 @@ static void set_attrs()
                          (int)kSolveSmem);
     cudaFuncSetAttribute(k_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSolveSmem);
+    cudaFuncSetAttribute(k_event_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kQueueBytes);
     g_attrs = true;
 }
 
@@ -1257,4 +1316,20 @@ cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s)
                                        params, kSolveSmem, s);
 }
 
+}  // namespace evd
+
+namespace evd {
+cudaError_t launch_event_probe(const double *xc, const double *yc, const double *t, long long n,
+                               const double *nu3, const double *den3, double cx, double cy,
+                               int W, int H, int blocks, int reps, unsigned long long *ctrs,
+                               unsigned long long *span, unsigned int *scratch, cudaStream_t s)
+{
+    set_attrs();
+    EventJob j{xc, yc, t, n, nu3[0], nu3[1], nu3[2], den3[0], den3[1], den3[2], cx, cy, W, H,
+               nullptr, nullptr, nullptr, kModeNode, nullptr,
+               (long long)blocks * kSolveThreads, 0};
+    k_event_probe<<<blocks, kSolveThreads, kQueueBytes, s>>>(j, reps, ctrs, span, scratch,
+                                                             (long long)W * H);
+    return cudaGetLastError();
+}
 }  // namespace evd

@@ -41,6 +41,9 @@ def main():
     cfg = int(args[0]) if args else 2
     reps = int(args[1]) if len(args) > 1 else 3
     b = synth.config_window(cfg)
+    if os.environ.get("EVD_SHUFFLE"):  # event order does not change any result
+        perm = np.random.default_rng(0).permutation(b.n)
+        b = type(b)(b.x[perm], b.y[perm], b.t[perm], b.tau, b.geometry)
     for _ in range(reps):
         r, st = sol.solve_window(b, evd.SolverParams())
     tr = trace(_lib.context())
