@@ -148,6 +148,21 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
                       const evd_solve_params *params, evd_window_result *results,
                       double *device_ms);
 
+/* batch_stream + estimate_stream_divergence (events.py:330-359,
+ * solver.py:139-162) for a whole time-sorted stream in one call: the raw
+ * events go to the device once, the windows [k*tau, (k+1)*tau) are found by
+ * binary search on the device, their events are gathered into the solve
+ * layout (centred x, y; batch-local t = min(t - k*tau, tau)) and every window
+ * is solved in one evd_solve_windows launch.  *n_windows = k1 - k0 + 1 (also
+ * on EVD_ERR_ARG when `capacity` is too small), *k0 = floor(t[0] / tau);
+ * results[w] describes window k0 + w (t_start = (k0 + w) * tau; status
+ * EVD_ERR_NO_EVENTS for an empty window).  The stream becomes the context's
+ * resident event set (as evd_set_events), windows concatenated. */
+int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                     int32_t width, int32_t height, double tau, int32_t groups,
+                     const evd_solve_params *params, evd_window_result *results,
+                     int32_t capacity, int32_t *n_windows, int64_t *k0, double *device_ms);
+
 /* Tracing is off unless the environment holds EVD_TRACE=1 when the context
  * is created (it costs a few percent).
  * Device timestamps (ns, %globaltimer) of the last solve (first window of

@@ -15,7 +15,7 @@ from .geometry import (CheiralityError, DivergenceSample, VelocityInterval,
                        velocity_domain, warp_batch, warp_scale)
 from .solver import (BnbResult, IterationLimitError, NoEventsError, SolverParams,
                      contrast_at, estimate_stream_divergence, grid_search_oracle,
-                     maximise_contrast_bnb)
+                     maximise_contrast_bnb, stream_divergence)
 from ._lib import EvdError, EvdUnavailable, set_device
 
 __version__ = "0.1.0"

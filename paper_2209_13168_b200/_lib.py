@@ -26,7 +26,7 @@ SYMBOLS = (
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
     "evd_rasterize_segments",
     "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
-    "evd_probe_events",
+    "evd_probe_events", "evd_solve_stream",
     "evd_pow2_table",
 )
 
@@ -95,6 +95,9 @@ _SIGS = {
     "evd_solve_trace": (ctypes.c_int, [_vp, _i64p, _i64, _i64p]),
     "evd_solve_block_trace": (ctypes.c_int, [_vp, _i64p, _i64, ctypes.POINTER(_i32)]),
     "evd_probe_events": (ctypes.c_int, [_vp, _f64, _f64, _i32, _d]),
+    "evd_solve_stream": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64, _i32,
+                                        ctypes.POINTER(SolveParams), ctypes.POINTER(WindowResult),
+                                        _i32, ctypes.POINTER(_i32), _i64p, _d]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
 }
 

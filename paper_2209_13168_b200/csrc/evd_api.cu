@@ -96,6 +96,8 @@ struct evd_ctx {
     DevBuf<WindowResult> wres;
     DevBuf<long long> trace, btrace;
     DevBuf<unsigned long long> probe_ctr, probe_span;  // evd_probe_events
+    DevBuf<double> sx, sy, st;        // raw stream (evd_solve_stream)
+    DevBuf<long long> wbounds;        // window lo, hi, offsets
     DevBuf<unsigned int> probe_img;
     long long trace_n = 0;
     bool trace_on = false;  // EVD_TRACE=1 at evd_create: record solve timelines
@@ -431,6 +433,10 @@ void evd_destroy(evd_ctx *ctx)
     ctx->probe_ctr.release();
     ctx->probe_span.release();
     ctx->probe_img.release();
+    ctx->sx.release();
+    ctx->sy.release();
+    ctx->st.release();
+    ctx->wbounds.release();
     TreePlan &tp = ctx->tree;
     tp.leaves.release();
     tp.cut_leaf0.release();
@@ -916,20 +922,13 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
     return EVD_OK;
 }
 
-int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, int32_t groups,
-                      const evd_solve_params *params, evd_window_result *results,
-                      double *device_ms)
+// Solve windows [offsets[w], offsets[w+1]) of the resident events (shared by
+// evd_solve_windows and evd_solve_stream).
+static int solve_offsets(evd_ctx *ctx, const long long *offsets, int n_windows, int groups,
+                         const evd_solve_params *params, evd_window_result *results,
+                         double *device_ms)
 {
-    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
-    if (!params || !results || !offsets || n_windows < 0)
-        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_windows arguments");
-    int rc = need_events(ctx);
-    if (rc) return rc;
-    if (n_windows == 0) return EVD_OK;
-    if (offsets[0] < 0 || offsets[n_windows] > ctx->n)
-        return fail(ctx, EVD_ERR_ARG, "window offsets outside the resident events");
-    for (int w = 0; w < n_windows; w++)
-        if (offsets[w + 1] < offsets[w]) return fail(ctx, EVD_ERR_ARG, "offsets must be non-decreasing");
+    int rc;
     if (groups <= 0) {
         // auto: ~20 events per thread per group, at least one window per group
         // (cfg4, 2000 windows of ~20k events: 74 groups of 2 CTAs measured best;
@@ -942,8 +941,7 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
     }
     std::vector<WindowResult> out;
     float ms = 0.f;
-    if ((rc = run_windows(ctx, (const long long *)offsets, n_windows, groups, params, out, &ms)))
-        return rc;
+    if ((rc = run_windows(ctx, offsets, n_windows, groups, params, out, &ms))) return rc;
     for (int w = 0; w < n_windows; w++) {
         evd_window_result &r = results[w];
         r.nu = out[w].nu;
@@ -962,6 +960,93 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
     }
     if (device_ms) *device_ms = ms;
     return EVD_OK;
+}
+
+int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, int32_t groups,
+                      const evd_solve_params *params, evd_window_result *results,
+                      double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !results || !offsets || n_windows < 0)
+        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_windows arguments");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    if (n_windows == 0) return EVD_OK;
+    if (offsets[0] < 0 || offsets[n_windows] > ctx->n)
+        return fail(ctx, EVD_ERR_ARG, "window offsets outside the resident events");
+    for (int w = 0; w < n_windows; w++)
+        if (offsets[w + 1] < offsets[w]) return fail(ctx, EVD_ERR_ARG, "offsets must be non-decreasing");
+    return solve_offsets(ctx, (const long long *)offsets, n_windows, groups, params, results,
+                         device_ms);
+}
+
+int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                     int32_t width, int32_t height, double tau, int32_t groups,
+                     const evd_solve_params *params, evd_window_result *results,
+                     int32_t capacity, int32_t *n_windows, int64_t *k0_out, double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !n_windows || !k0_out || n < 0 || width < 1 || height < 1)
+        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_stream arguments");
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "tau must be positive");
+    *n_windows = 0;
+    *k0_out = 0;
+    if (device_ms) *device_ms = 0.0;
+    if (n == 0) return EVD_OK;  // batch_stream of an empty stream: no windows
+    if (!x || !y || !t) return fail(ctx, EVD_ERR_ARG, "NULL event array");
+    // events.py:341-342: k0 = int(floor(t[0] / tau)), k1 = int(floor(t[-1] / tau))
+    const double f0 = std::floor(t[0] / tau), f1 = std::floor(t[n - 1] / tau);
+    if (!(f0 >= 0.0) || !(f1 >= f0) || f1 - f0 >= 2147483647.0)
+        return fail(ctx, EVD_ERR_ARG, "timestamps must be sorted, non-negative and finite");
+    const long long k0 = (long long)f0;
+    const int nw = (int)((long long)f1 - k0 + 1);
+    *n_windows = nw;
+    *k0_out = k0;
+    if (!results || capacity < nw)
+        return fail(ctx, EVD_ERR_ARG, "stream spans %d windows, results hold %d", nw, capacity);
+    CU(cudaSetDevice(ctx->device));
+    // raw stream -> device, window bounds by binary search on the device
+    CU(ctx->sx.ensure(n));
+    CU(ctx->sy.ensure(n));
+    CU(ctx->st.ensure(n));
+    CU(ctx->wbounds.ensure(3 * (size_t)nw + 1));
+    CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    long long *lo = ctx->wbounds.p, *hi = lo + nw, *off = hi + nw;
+    launch_window_bounds(ctx->st.p, n, k0, nw, tau, lo, hi, ctx->stream);
+    LAUNCHED(1);
+    std::vector<long long> h(2 * (size_t)nw), o(nw + 1);
+    CU(cudaMemcpyAsync(h.data(), lo, 2 * nw * sizeof(long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    o[0] = 0;
+    for (int w = 0; w < nw; w++) o[w + 1] = o[w] + std::max(0LL, h[nw + w] - h[w]);
+    const long long total = o[nw];
+    // the windows' events, concatenated in the solve layout
+    CU(ctx->xc.ensure(std::max(total, 1LL)));
+    CU(ctx->yc.ensure(std::max(total, 1LL)));
+    CU(ctx->t.ensure(std::max(total, 1LL)));
+    CU(cudaMemcpyAsync(off, o.data(), (nw + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if (total > 0) {
+        launch_gather_windows(ctx->sx.p, ctx->sy.p, ctx->st.p, lo, off, nw, k0, total, tau,
+                              width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p, ctx->t.p,
+                              ctx->stream);
+        LAUNCHED(1);
+    }
+    ctx->n = total;
+    ctx->W = width;
+    ctx->H = height;
+    ctx->tau = tau;
+    if (total == 0) {  // every window empty
+        for (int w = 0; w < nw; w++) {
+            results[w] = evd_window_result{};
+            results[w].status = EVD_ERR_NO_EVENTS;
+        }
+        return EVD_OK;
+    }
+    return solve_offsets(ctx, o.data(), nw, groups, params, results, device_ms);
 }
 
 int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n)

@@ -139,6 +139,12 @@ void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, 
 int solve_grid_blocks(int device);
 int solve_block_threads();
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
+void launch_window_bounds(const double *t, long long n, long long k0, int nw, double tau,
+                          long long *lo, long long *hi, cudaStream_t s);
+void launch_gather_windows(const double *x, const double *y, const double *t,
+                           const long long *lo, const long long *off, int nw, long long k0,
+                           long long total, double tau, double cx, double cy, double *xc,
+                           double *yc, double *tl, cudaStream_t s);
 cudaError_t launch_event_probe(const double *xc, const double *yc, const double *t, long long n,
                                const double *nu3, const double *den3, double cx, double cy,
                                int W, int H, int blocks, int reps, unsigned long long *ctrs,

@@ -1333,3 +1333,75 @@ cudaError_t launch_event_probe(const double *xc, const double *yc, const double 
     return cudaGetLastError();
 }
 }  // namespace evd
+
+// ---------------------------------------------------------------- stream windowing
+namespace evd {
+
+// First index i in [0, n) with t[i] >= v (numpy searchsorted side="left").
+__device__ __forceinline__ long long lower_bound_f64(const double *t, long long n, double v)
+{
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (__ldg(t + mid) < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// batch_stream window bounds (events.py:341-347): window w is k = k0 + w,
+// start = k * tau (Python int * float), events [searchsorted(start),
+// searchsorted(start + tau)) of the time-sorted stream.
+__global__ void k_window_bounds(const double *__restrict__ t, long long n, long long k0, int nw,
+                                double tau, long long *__restrict__ lo, long long *__restrict__ hi)
+{
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+        const double start = dmul((double)(k0 + w), tau);
+        lo[w] = lower_bound_f64(t, n, start);
+        hi[w] = lower_bound_f64(t, n, dadd(start, tau));
+    }
+}
+
+// Concatenate the windows' events into the solve layout: centred x, y
+// (geometry.py:87) and batch-local t = min(t - start, tau) (events.py:348).
+__global__ void k_gather_windows(const double *__restrict__ x, const double *__restrict__ y,
+                                 const double *__restrict__ t, const long long *__restrict__ lo,
+                                 const long long *__restrict__ off, int nw, long long k0,
+                                 double tau, double cx, double cy, double *__restrict__ xc,
+                                 double *__restrict__ yc, double *__restrict__ tl)
+{
+    const long long total = off[nw];
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total;
+         j += (long long)gridDim.x * blockDim.x) {
+        int a = 0, b = nw;  // largest w with off[w] <= j
+        while (b - a > 1) {
+            const int m = (a + b) >> 1;
+            if (__ldg(off + m) <= j) a = m;
+            else b = m;
+        }
+        const long long i = __ldg(lo + a) + (j - __ldg(off + a));
+        const double start = dmul((double)(k0 + a), tau);
+        xc[j] = dsub(__ldg(x + i), cx);
+        yc[j] = dsub(__ldg(y + i), cy);
+        const double d = dsub(__ldg(t + i), start);
+        tl[j] = d < tau ? d : tau;
+    }
+}
+
+void launch_window_bounds(const double *t, long long n, long long k0, int nw, double tau,
+                          long long *lo, long long *hi, cudaStream_t s)
+{
+    const int blocks = std::max(1, std::min((nw + 255) / 256, num_sms() * 4));
+    k_window_bounds<<<blocks, 256, 0, s>>>(t, n, k0, nw, tau, lo, hi);
+}
+
+void launch_gather_windows(const double *x, const double *y, const double *t,
+                           const long long *lo, const long long *off, int nw, long long k0,
+                           long long total, double tau, double cx, double cy, double *xc,
+                           double *yc, double *tl, cudaStream_t s)
+{
+    k_gather_windows<<<event_blocks(total), kThreads, 0, s>>>(x, y, t, lo, off, nw, k0, tau, cx,
+                                                               cy, xc, yc, tl);
+}
+
+}  // namespace evd

@@ -211,6 +211,63 @@ def estimate_stream_divergence(batches: list[EventBatch], params: SolverParams
     return samples
 
 
+def stream_divergence(stream, params: SolverParams, tau: float | None = None, groups: int = 0,
+                      ctx=None) -> list[DivergenceSample]:
+    """``estimate_stream_divergence(batch_stream(stream, tau), params)`` in one
+    device call (evd_solve_stream): windowing (events.py:330-359) on the device,
+    then every window solved in one launch.  ``tau`` defaults to ``params.tau``.
+
+    The samples equal the host pipeline's (t = window end, divergence, contrast,
+    bound_gap, iterations); empty windows leave a gap and an iteration-limited
+    window is logged and skipped, as solver.py:148-160 does.  ``runtime`` is
+    the call's wall time divided evenly over the solved windows.
+    """
+    tau = float(params.tau if tau is None else tau)
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    n = len(stream.t)
+    if n == 0:
+        return []
+    velocity_domain(tau, params.epsilon)
+    x, y, t = _lib.f64(stream.x), _lib.f64(stream.y), _lib.f64(stream.t)
+    k0 = int(np.floor(t[0] / tau))
+    cap = int(np.floor(t[-1] / tau)) - k0 + 1
+    ctx = ctx or _lib.context()
+    g = stream.geometry
+    p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
+                         float(params.min_interval_width), int(params.max_iterations))
+    res = (_lib.WindowResult * cap)()
+    nw = ctypes.c_int32()
+    k0_dev = ctypes.c_int64()
+    ms = (ctypes.c_double * 1)()
+    start = time.perf_counter()
+    rc = ctx.lib.evd_solve_stream(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t), n, g.width,
+                                  g.height, tau, int(groups), p, res, cap, ctypes.byref(nw),
+                                  ctypes.byref(k0_dev), ms)
+    if rc:
+        _raise(ctx, rc)
+    wall = time.perf_counter() - start
+    solved = sum(1 for r in res[: nw.value] if r.status == _lib.EVD_OK)
+    per = wall / max(solved, 1)
+    samples = []
+    for w in range(nw.value):
+        r = res[w]
+        t_start = (k0_dev.value + w) * tau  # events.py:345
+        if r.status == _lib.EVD_ERR_NO_EVENTS:
+            continue
+        if r.status == _lib.EVD_ERR_ITER_LIMIT:
+            LOG.warning("batch at t=%.3f s: %s", t_start,
+                        IterationLimitError(r.nu, r.contrast, int(r.iterations)))
+            continue
+        if r.status != _lib.EVD_OK:
+            raise _lib.EvdError(r.status, f"window at t={t_start}: status {r.status}")
+        samples.append(DivergenceSample(
+            t=t_start + tau, divergence=divergence_from_velocity(r.nu, tau),
+            contrast=r.contrast, bound_gap=r.bound_gap, iterations=int(r.iterations),
+            runtime=per))
+    return samples
+
+
 def _estimate_each(batches: list[EventBatch], params: SolverParams) -> list[DivergenceSample]:
     samples = []
     for batch in batches:

@@ -74,6 +74,16 @@ def landing_stream(d: Descent) -> EventStream:
     return EventStream(x[order], y[order], t[order], pol[order], g)
 
 
+def concat_streams(streams: list[EventStream], period: float) -> EventStream:
+    """One time-sorted stream from several, stream i shifted by i * period
+    (a long landing sequence for the stream pipeline; each part must end
+    before ``period``)."""
+    g = streams[0].geometry
+    parts = [(s.x, s.y, s.t + i * period, s.polarity) for i, s in enumerate(streams)]
+    cat = lambda k: np.concatenate([p[k] for p in parts])
+    return EventStream(cat(0), cat(1), cat(2), cat(3), g)
+
+
 def stream_windows(stream: EventStream, tau: float = 0.5) -> list[EventBatch]:
     """All windows of a stream (including empty ones), as ``batch_stream``."""
     k0, bounds = window_bounds(stream.t, tau)

@@ -1,0 +1,61 @@
+"""Whole-stream pipeline on the device (evd_solve_stream)
+against the host pipeline estimate_stream_divergence(batch_stream(...)), which
+the window tests pin to the reference, and against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+import paper_2209_13168_b200 as evd
+from paper_2209_13168_b200 import synth
+from paper_2209_13168_b200.events import EventStream
+from paper_2209_13168_b200.geometry import divergence_from_velocity
+
+pytestmark = pytest.mark.gpu
+
+
+def _key(samples):
+    return [(s.t, s.divergence, s.contrast, s.bound_gap, s.iterations) for s in samples]
+
+
+def _stream(n_desc=3, w=96, h=72, pts=300, seed=5):
+    parts = [synth.landing_stream(synth.Descent(w, h, pts, nu=-0.1 - 0.15 * i, duration=2.0,
+                                                seed=seed + i)) for i in range(n_desc)]
+    return synth.concat_streams(parts, 2.0)
+
+
+@pytest.mark.parametrize("tau", [0.5, 0.3, 0.7])
+def test_stream_matches_host_pipeline(tau):
+    s = _stream()
+    params = evd.SolverParams(tau=tau)
+    host = evd.estimate_stream_divergence(evd.batch_stream(s, tau), params)
+    dev = evd.stream_divergence(s, params)
+    assert len(dev) > 4
+    assert _key(dev) == _key(host)
+
+
+def test_stream_matches_oracle():
+    s = _stream(n_desc=2, w=64, h=48, pts=150)
+    params = evd.SolverParams()
+    dev = evd.stream_divergence(s, params)
+    ref = []
+    for b in evd.batch_stream(s, 0.5):
+        if b.n == 0:
+            continue
+        r = orc.maximise_contrast_bnb(b)
+        ref.append((b.t_end, divergence_from_velocity(r.nu, b.tau), r.contrast, r.bound_gap,
+                    r.iterations))
+    assert _key(dev) == ref
+
+
+def test_stream_gaps_offset_start_and_iteration_limit():
+    s = _stream()
+    keep = (s.t < 1.2) | (s.t >= 2.9)  # windows [1.5, 2.0), [2.0, 2.5) become empty
+    keep &= s.t >= 0.6                 # stream starts in window k0 = 1
+    g = EventStream(s.x[keep], s.y[keep], s.t[keep], s.polarity[keep], s.geometry)
+    for params in (evd.SolverParams(), evd.SolverParams(max_iterations=3)):
+        host = evd.estimate_stream_divergence(evd.batch_stream(g, 0.5), params)
+        dev = evd.stream_divergence(g, params)
+        assert _key(dev) == _key(host)
+    assert evd.stream_divergence(EventStream(np.empty(0), np.empty(0), np.empty(0),
+                                             np.empty(0), s.geometry), evd.SolverParams()) == []
