@@ -37,7 +37,9 @@ enum {
     EVD_ERR_NO_EVENTS = 3,    /* NoEventsError, solver.py:32-33,88-89 */
     EVD_ERR_CHEIRALITY = 4,   /* CheiralityError, geometry.py:21-22,72-74 (1 + nu*tau <= 0) */
     EVD_ERR_ITER_LIMIT = 5,   /* IterationLimitError, solver.py:36-46,118-119; result holds the incumbent */
-    EVD_ERR_STATE = 6         /* call order (e.g. no events set) */
+    EVD_ERR_STATE = 6,        /* call order (e.g. no events set) */
+    EVD_ERR_FORMAT = 7,       /* malformed EVD1 file (EventFormatError, events.py:186-201) */
+    EVD_ERR_VALIDATION = 8    /* stream invariant violated (EventValidationError, events.py:61-81) */
 };
 
 /* ---- context ----------------------------------------------------------- */
@@ -162,6 +164,26 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
                      int32_t width, int32_t height, double tau, int32_t groups,
                      const evd_solve_params *params, evd_window_result *results,
                      int32_t capacity, int32_t *n_windows, int64_t *k0, double *device_ms);
+
+/* Same pipeline on the stream already resident in the context (the last
+ * evd_solve_stream upload or evd_load_bin). */
+int evd_solve_loaded_stream(evd_ctx *ctx, double tau, int32_t groups,
+                            const evd_solve_params *params, evd_window_result *results,
+                            int32_t capacity, int32_t *n_windows, int64_t *k0,
+                            double *device_ms);
+
+/* ---- EVD1 event files ------------------------------ */
+/* parse_event_bin (events.py:186-206) + _from_columns (:128-134) on the
+ * device: the 20-byte <4sIIQ> header is checked on the host, the packed
+ * 17-byte records <u8 t_us, f4 x, f4 y, i1 p> are copied once and decoded on
+ * the device (t = float64(t_us) * 1e-6, x, y widened exactly), stably sorted
+ * by t when out of order, and checked against the EventStream invariants
+ * (EVD_ERR_VALIDATION with the reference's message).  The stream stays
+ * resident for evd_solve_loaded_stream / evd_stream_copy. */
+int evd_load_bin(evd_ctx *ctx, const uint8_t *data, int64_t size, int32_t *width,
+                 int32_t *height, int64_t *n);
+/* Copy the resident stream to host arrays of n elements (any may be NULL). */
+int evd_stream_copy(evd_ctx *ctx, double *x, double *y, double *t, int8_t *p);
 
 /* Tracing is off unless the environment holds EVD_TRACE=1 when the context
  * is created (it costs a few percent).

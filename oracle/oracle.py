@@ -225,3 +225,45 @@ def grid_search(batch, n_points, epsilon=1e-6):
     cs = np.array([contrast_at(batch, float(nu)) for nu in nus])
     best = int(np.argmax(cs))
     return float(nus[best]), float(cs[best])
+
+
+# ------------------------------------------------------------------ EVD1 files
+class FormatError(ValueError):
+    pass
+
+
+class ValidationError(ValueError):
+    pass
+
+
+def parse_bin(data: bytes):
+    """parse_event_bin (events.py:186-206) + _from_columns (:128-134) + the
+    EventStream invariants (:61-81), restated with numpy/struct.  Returns
+    (x, y, t, p, (width, height)); raises FormatError / ValidationError with
+    the reference's messages."""
+    import struct
+    if len(data) < 20:
+        raise FormatError("truncated BIN header")
+    magic, width, height, count = struct.unpack_from("<4sIIQ", data, 0)
+    if magic != b"EVD1":
+        raise FormatError(f"bad magic {magic!r}")
+    rec = np.dtype([("t_us", "<u8"), ("x", "<f4"), ("y", "<f4"), ("p", "i1")])
+    if len(data) < 20 + count * rec.itemsize:
+        raise FormatError(f"truncated BIN body: expected {count} records")
+    r = np.frombuffer(data, dtype=rec, count=count, offset=20)
+    if width < 1 or height < 1:
+        raise ValidationError(f"sensor dimensions must be positive, got {width}x{height}")
+    t = np.asarray(r["t_us"], dtype=np.float64) * 1e-6
+    order = np.argsort(t, kind="stable")
+    x = np.asarray(r["x"], np.float64)[order]
+    y = np.asarray(r["y"], np.float64)[order]
+    t = t[order]
+    p = np.asarray(r["p"], np.int8)[order]
+    if len(t):
+        if not (np.isfinite(x).all() and np.isfinite(y).all()):
+            raise ValidationError("event coordinates must be finite")
+        if ((x < 0) | (x >= width) | (y < 0) | (y >= height)).any():
+            raise ValidationError("event coordinates outside sensor geometry")
+        if not np.isin(p, (-1, 1)).all():
+            raise ValidationError("polarity must be +1 or -1")
+    return x, y, t, p, (int(width), int(height))

@@ -9,13 +9,14 @@ solver, computed by hand-written sm_100a CUDA (libevd.so, include/evd.h).
 from .contrast import (ContrastBound, EventImage, accumulate_image, bound_terms,
                        image_contrast, image_contrast_expanded, rasterize_segment,
                        upper_bound_image)
-from .events import EventBatch, EventStream, EventValidationError, SensorGeometry, batch_stream
+from .events import (BIN_MAGIC, EventBatch, EventFormatError, EventStream, EventValidationError,
+                     SensorGeometry, batch_stream, parse_event_bin, write_event_bin)
 from .geometry import (CheiralityError, DivergenceSample, VelocityInterval,
                        continuous_divergence, divergence_from_velocity, radial_warp,
                        velocity_domain, warp_batch, warp_scale)
 from .solver import (BnbResult, IterationLimitError, NoEventsError, SolverParams,
                      contrast_at, estimate_stream_divergence, grid_search_oracle,
-                     maximise_contrast_bnb, stream_divergence)
+                     maximise_contrast_bnb, stream_divergence, stream_divergence_bin)
 from ._lib import EvdError, EvdUnavailable, set_device
 
 __version__ = "0.1.0"

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("EVD_LIB") or os.path.join(HERE, "libevd.so")
 
 EVD_OK, EVD_ERR_CUDA, EVD_ERR_ARG, EVD_ERR_NO_EVENTS = 0, 1, 2, 3
 EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
+EVD_ERR_FORMAT, EVD_ERR_VALIDATION = 7, 8
 
 # every symbol include/evd.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
@@ -26,7 +27,8 @@ SYMBOLS = (
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
     "evd_rasterize_segments",
     "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
-    "evd_probe_events", "evd_solve_stream",
+    "evd_probe_events", "evd_solve_stream", "evd_solve_loaded_stream", "evd_load_bin",
+    "evd_stream_copy",
     "evd_pow2_table",
 )
 
@@ -98,6 +100,12 @@ _SIGS = {
     "evd_solve_stream": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64, _i32,
                                         ctypes.POINTER(SolveParams), ctypes.POINTER(WindowResult),
                                         _i32, ctypes.POINTER(_i32), _i64p, _d]),
+    "evd_solve_loaded_stream": (ctypes.c_int, [_vp, _f64, _i32, ctypes.POINTER(SolveParams),
+                                               ctypes.POINTER(WindowResult), _i32,
+                                               ctypes.POINTER(_i32), _i64p, _d]),
+    "evd_load_bin": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64, ctypes.POINTER(_i32),
+                                    ctypes.POINTER(_i32), _i64p]),
+    "evd_stream_copy": (ctypes.c_int, [_vp, _d, _d, _d, ctypes.POINTER(ctypes.c_int8)]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
 }
 

@@ -96,7 +96,13 @@ struct evd_ctx {
     DevBuf<WindowResult> wres;
     DevBuf<long long> trace, btrace;
     DevBuf<unsigned long long> probe_ctr, probe_span;  // evd_probe_events
-    DevBuf<double> sx, sy, st;        // raw stream (evd_solve_stream)
+    DevBuf<double> sx, sy, st;        // resident raw stream (evd_solve_stream, evd_load_bin)
+    DevBuf<signed char> sp;           // its polarity (evd_load_bin)
+    DevBuf<unsigned char> sbytes, sscratch;  // EVD1 body, decode scratch
+    DevBuf<unsigned int> sflags;
+    long long sn = -1;                // resident stream length (-1: none)
+    int sW = 0, sH = 0;
+    bool s_has_p = false;
     DevBuf<long long> wbounds;        // window lo, hi, offsets
     DevBuf<unsigned int> probe_img;
     long long trace_n = 0;
@@ -437,6 +443,10 @@ void evd_destroy(evd_ctx *ctx)
     ctx->sy.release();
     ctx->st.release();
     ctx->wbounds.release();
+    ctx->sp.release();
+    ctx->sbytes.release();
+    ctx->sscratch.release();
+    ctx->sflags.release();
     TreePlan &tp = ctx->tree;
     tp.leaves.release();
     tp.cut_leaf0.release();
@@ -980,22 +990,25 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
                          device_ms);
 }
 
-int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
-                     int32_t width, int32_t height, double tau, int32_t groups,
-                     const evd_solve_params *params, evd_window_result *results,
-                     int32_t capacity, int32_t *n_windows, int64_t *k0_out, double *device_ms)
+// Windows of the resident raw stream (sx, sy, st: time-sorted, sn events):
+// bounds by device binary search, gather into the solve layout, one solve.
+static int solve_resident_stream(evd_ctx *ctx, double tau, int groups,
+                                 const evd_solve_params *params, evd_window_result *results,
+                                 int capacity, int32_t *n_windows, int64_t *k0_out,
+                                 double *device_ms)
 {
-    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
-    if (!params || !n_windows || !k0_out || n < 0 || width < 1 || height < 1)
-        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_stream arguments");
-    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "tau must be positive");
     *n_windows = 0;
     *k0_out = 0;
     if (device_ms) *device_ms = 0.0;
+    const long long n = ctx->sn;
     if (n == 0) return EVD_OK;  // batch_stream of an empty stream: no windows
-    if (!x || !y || !t) return fail(ctx, EVD_ERR_ARG, "NULL event array");
+    double tt[2];
+    CU(cudaMemcpyAsync(tt, ctx->st.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(tt + 1, ctx->st.p + n - 1, sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     // events.py:341-342: k0 = int(floor(t[0] / tau)), k1 = int(floor(t[-1] / tau))
-    const double f0 = std::floor(t[0] / tau), f1 = std::floor(t[n - 1] / tau);
+    const double f0 = std::floor(tt[0] / tau), f1 = std::floor(tt[1] / tau);
     if (!(f0 >= 0.0) || !(f1 >= f0) || f1 - f0 >= 2147483647.0)
         return fail(ctx, EVD_ERR_ARG, "timestamps must be sorted, non-negative and finite");
     const long long k0 = (long long)f0;
@@ -1004,15 +1017,7 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
     *k0_out = k0;
     if (!results || capacity < nw)
         return fail(ctx, EVD_ERR_ARG, "stream spans %d windows, results hold %d", nw, capacity);
-    CU(cudaSetDevice(ctx->device));
-    // raw stream -> device, window bounds by binary search on the device
-    CU(ctx->sx.ensure(n));
-    CU(ctx->sy.ensure(n));
-    CU(ctx->st.ensure(n));
     CU(ctx->wbounds.ensure(3 * (size_t)nw + 1));
-    CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     long long *lo = ctx->wbounds.p, *hi = lo + nw, *off = hi + nw;
     launch_window_bounds(ctx->st.p, n, k0, nw, tau, lo, hi, ctx->stream);
     LAUNCHED(1);
@@ -1031,13 +1036,13 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
                        ctx->stream));
     if (total > 0) {
         launch_gather_windows(ctx->sx.p, ctx->sy.p, ctx->st.p, lo, off, nw, k0, total, tau,
-                              width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p, ctx->t.p,
+                              ctx->sW / 2.0, ctx->sH / 2.0, ctx->xc.p, ctx->yc.p, ctx->t.p,
                               ctx->stream);
         LAUNCHED(1);
     }
     ctx->n = total;
-    ctx->W = width;
-    ctx->H = height;
+    ctx->W = ctx->sW;
+    ctx->H = ctx->sH;
     ctx->tau = tau;
     if (total == 0) {  // every window empty
         for (int w = 0; w < nw; w++) {
@@ -1047,6 +1052,131 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
         return EVD_OK;
     }
     return solve_offsets(ctx, o.data(), nw, groups, params, results, device_ms);
+}
+
+int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                     int32_t width, int32_t height, double tau, int32_t groups,
+                     const evd_solve_params *params, evd_window_result *results,
+                     int32_t capacity, int32_t *n_windows, int64_t *k0_out, double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !n_windows || !k0_out || n < 0 || width < 1 || height < 1)
+        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_stream arguments");
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "tau must be positive");
+    if (n > 0 && (!x || !y || !t)) return fail(ctx, EVD_ERR_ARG, "NULL event array");
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->sx.ensure(std::max(n, (int64_t)1)));
+    CU(ctx->sy.ensure(std::max(n, (int64_t)1)));
+    CU(ctx->st.ensure(std::max(n, (int64_t)1)));
+    if (n > 0) {
+        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->sn = n;
+    ctx->sW = width;
+    ctx->sH = height;
+    ctx->s_has_p = false;
+    return solve_resident_stream(ctx, tau, groups, params, results, capacity, n_windows, k0_out,
+                                 device_ms);
+}
+
+int evd_solve_loaded_stream(evd_ctx *ctx, double tau, int32_t groups,
+                            const evd_solve_params *params, evd_window_result *results,
+                            int32_t capacity, int32_t *n_windows, int64_t *k0_out,
+                            double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!params || !n_windows || !k0_out) return fail(ctx, EVD_ERR_ARG, "bad arguments");
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "tau must be positive");
+    if (ctx->sn < 0) return fail(ctx, EVD_ERR_STATE, "no stream loaded (evd_load_bin)");
+    CU(cudaSetDevice(ctx->device));
+    return solve_resident_stream(ctx, tau, groups, params, results, capacity, n_windows, k0_out,
+                                 device_ms);
+}
+
+int evd_load_bin(evd_ctx *ctx, const uint8_t *data, int64_t size, int32_t *width,
+                 int32_t *height, int64_t *n_out)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!width || !height || !n_out || (size > 0 && !data) || size < 0)
+        return fail(ctx, EVD_ERR_ARG, "bad evd_load_bin arguments");
+    // header <4sIIQ> (events.py:188-193)
+    if (size < 20) return fail(ctx, EVD_ERR_FORMAT, "truncated BIN header");
+    if (std::memcmp(data, "EVD1", 4) != 0) {
+        char m[64];
+        int k = 0;
+        for (int i = 0; i < 4; i++) {
+            const unsigned char c = data[i];
+            if (c >= 32 && c < 127 && c != '\\' && c != '\'') m[k++] = (char)c;
+            else k += std::snprintf(m + k, sizeof(m) - k, "\\x%02x", c);
+        }
+        m[k] = 0;
+        return fail(ctx, EVD_ERR_FORMAT, "bad magic b'%s'", m);
+    }
+    uint32_t w, h;
+    uint64_t count;
+    std::memcpy(&w, data + 4, 4);
+    std::memcpy(&h, data + 8, 4);
+    std::memcpy(&count, data + 12, 8);
+    if (count > (uint64_t)(size - 20) / 17)  // events.py:197-201
+        return fail(ctx, EVD_ERR_FORMAT, "truncated BIN body: expected %llu records",
+                    (unsigned long long)count);
+    if (w < 1 || h < 1 || w > 2147483647u || h > 2147483647u)  // SensorGeometry (events.py:37-39)
+        return fail(ctx, EVD_ERR_VALIDATION, "sensor dimensions must be positive, got %ux%u", w, h);
+    const long long n = (long long)count;
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->sx.ensure(std::max(n, 1LL)));
+    CU(ctx->sy.ensure(std::max(n, 1LL)));
+    CU(ctx->st.ensure(std::max(n, 1LL)));
+    CU(ctx->sp.ensure(std::max(n, 1LL)));
+    ctx->sn = -1;
+    if (n > 0) {
+        CU(ctx->sbytes.ensure((size_t)n * 17));
+        const size_t scratch = decode_scratch_bytes(n);
+        CU(ctx->sscratch.ensure(scratch));
+        CU(ctx->sflags.ensure(1));
+        CU(cudaMemcpyAsync(ctx->sbytes.p, data + 20, (size_t)n * 17, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        unsigned int flags = 0;
+        int launches = 0;
+        cudaError_t e = decode_bin(ctx->sbytes.p, n, (int)w, (int)h, ctx->sx.p, ctx->sy.p,
+                                   ctx->st.p, ctx->sp.p, ctx->sscratch.p, ctx->sscratch.cap,
+                                   ctx->sflags.p, &flags, &launches, ctx->stream);
+        ctx->launches += launches;
+        if (e != cudaSuccess) return fail(ctx, EVD_ERR_CUDA, "decode_bin: %s", cudaGetErrorString(e));
+        // EventStream invariants, in the reference's order (events.py:67-81)
+        if (flags & 2u) return fail(ctx, EVD_ERR_VALIDATION, "event coordinates must be finite");
+        if (flags & 4u)
+            return fail(ctx, EVD_ERR_VALIDATION, "event coordinates outside sensor geometry");
+        if (flags & 8u) return fail(ctx, EVD_ERR_VALIDATION, "polarity must be +1 or -1");
+    }
+    ctx->sn = n;
+    ctx->sW = (int)w;
+    ctx->sH = (int)h;
+    ctx->s_has_p = true;
+    *width = (int32_t)w;
+    *height = (int32_t)h;
+    *n_out = n;
+    return EVD_OK;
+}
+
+int evd_stream_copy(evd_ctx *ctx, double *x, double *y, double *t, int8_t *p)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (ctx->sn < 0) return fail(ctx, EVD_ERR_STATE, "no stream loaded");
+    const long long n = ctx->sn;
+    if (n == 0) return EVD_OK;
+    CU(cudaSetDevice(ctx->device));
+    if (x) CU(cudaMemcpyAsync(x, ctx->sx.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (y) CU(cudaMemcpyAsync(y, ctx->sy.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (t) CU(cudaMemcpyAsync(t, ctx->st.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (p) {
+        if (!ctx->s_has_p) return fail(ctx, EVD_ERR_STATE, "the loaded stream has no polarity");
+        CU(cudaMemcpyAsync(p, ctx->sp.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EVD_OK;
 }
 
 int evd_solve_trace(evd_ctx *ctx, int64_t *out, int64_t cap, int64_t *n)

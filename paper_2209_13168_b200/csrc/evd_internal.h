@@ -139,6 +139,11 @@ void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, 
 int solve_grid_blocks(int device);
 int solve_block_threads();
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
+cudaError_t decode_bin(const unsigned char *body_dev, long long n, int W, int H, double *x,
+                       double *y, double *t, signed char *p, void *scratch, size_t scratch_bytes,
+                       unsigned int *flags_dev, unsigned int *flags_host, int *launches,
+                       cudaStream_t s);
+size_t decode_scratch_bytes(long long n);
 void launch_window_bounds(const double *t, long long n, long long k0, int nw, double tau,
                           long long *lo, long long *hi, cudaStream_t s);
 void launch_gather_windows(const double *x, const double *y, const double *t,

@@ -8,20 +8,31 @@ pass them unchanged (every entry point in this package duck-types on the fields
 * ``EventStream``     -- ``pkg/src/eventdiv/events.py:47-90`` (validation rules kept)
 * ``EventBatch``      -- ``pkg/src/eventdiv/events.py:93-120``
 * ``batch_stream``    -- ``pkg/src/eventdiv/events.py:330-359`` (windowing)
+* ``parse_event_bin`` -- ``pkg/src/eventdiv/events.py:186-206`` (EVD1 decoded on the
+  device); ``write_event_bin`` (``:236-246``) for round trips
 
-File parsing, hot-pixel removal, rescaling and subsampling are outside the hot
+CSV parsing, hot-pixel removal, rescaling and subsampling are outside the hot
 path and are not provided here.
 """
 
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
+
+BIN_MAGIC = b"EVD1"
+_BIN_RECORD = np.dtype([("t_us", "<u8"), ("x", "<f4"), ("y", "<f4"), ("p", "i1")])
 
 
 class EventValidationError(ValueError):
     """Event data violates a stream/batch invariant (``events.py:25-26``)."""
+
+
+class EventFormatError(ValueError):
+    """Malformed event file (``events.py:21-22``)."""
 
 
 @dataclass(frozen=True)
@@ -130,3 +141,53 @@ def batch_stream(stream: EventStream, tau: float) -> list[EventBatch]:
             np.minimum(stream.t[lo:hi] - start, tau), tau, stream.geometry,
             t_start=start))
     return out
+
+
+def load_bin_resident(data: bytes, ctx=None):
+    """Decode an EVD1 body on the device (evd_load_bin); the stream stays
+    resident in the context.  Returns (ctx, geometry, n)."""
+    import ctypes
+
+    from . import _lib
+    ctx = ctx or _lib.context()
+    data = bytes(data)
+    w, h, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    rc = ctx.lib.evd_load_bin(ctx.h, data, len(data), ctypes.byref(w), ctypes.byref(h),
+                              ctypes.byref(n))
+    if rc == _lib.EVD_ERR_FORMAT:
+        raise EventFormatError(ctx.error_text())
+    if rc == _lib.EVD_ERR_VALIDATION:
+        raise EventValidationError(ctx.error_text())
+    if rc:
+        raise _lib.EvdError(rc, ctx.error_text())
+    return ctx, SensorGeometry(w.value, h.value), n.value
+
+
+def parse_event_bin(data: bytes, ctx=None) -> EventStream:
+    """Parse the BIN event format (``events.py:186-206``): decoded, sorted and
+    validated on the device, then copied back as an EventStream."""
+    import ctypes
+
+    from . import _lib
+    ctx, geometry, n = load_bin_resident(data, ctx)
+    x, y, t = (np.empty(n, dtype=np.float64) for _ in range(3))
+    p = np.empty(n, dtype=np.int8)
+    if n:
+        rc = ctx.lib.evd_stream_copy(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t),
+                                     p.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+        if rc:
+            raise _lib.EvdError(rc, ctx.error_text())
+    return EventStream(x, y, t, p, geometry)
+
+
+def write_event_bin(stream: EventStream, path) -> None:
+    """Write the BIN event format (``events.py:236-246``)."""
+    g = stream.geometry
+    body = np.empty(stream.n, dtype=_BIN_RECORD)
+    body["t_us"] = np.round(stream.t * 1e6).astype(np.uint64)
+    body["x"] = stream.x
+    body["y"] = stream.y
+    body["p"] = stream.polarity
+    with open(Path(path), "wb") as fh:
+        fh.write(struct.pack("<4sIIQ", BIN_MAGIC, g.width, g.height, stream.n))
+        fh.write(body.tobytes())

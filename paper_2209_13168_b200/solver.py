@@ -246,13 +246,54 @@ def stream_divergence(stream, params: SolverParams, tau: float | None = None, gr
                                   ctypes.byref(k0_dev), ms)
     if rc:
         _raise(ctx, rc)
-    wall = time.perf_counter() - start
-    solved = sum(1 for r in res[: nw.value] if r.status == _lib.EVD_OK)
+    return _samples(res, nw.value, k0_dev.value, tau, time.perf_counter() - start)
+
+
+def stream_divergence_bin(data: bytes, params: SolverParams, tau: float | None = None,
+                          groups: int = 0, ctx=None) -> list[DivergenceSample]:
+    """EVD1 file body -> divergence samples without a host parse: the records
+    are decoded on the device (evd_load_bin) and the resident stream is
+    windowed and solved there (evd_solve_loaded_stream).  Equals
+    ``estimate_stream_divergence(batch_stream(parse_event_bin(data), tau), params)``."""
+    from .events import load_bin_resident
+    tau = float(params.tau if tau is None else tau)
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    velocity_domain(tau, params.epsilon)
+    start = time.perf_counter()
+    ctx, _, n = load_bin_resident(data, ctx)
+    if n == 0:
+        return []
+    return _solve_resident(ctx, tau, params, groups, start)
+
+
+def _solve_resident(ctx, tau, params, groups, start):
+    p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
+                         float(params.min_interval_width), int(params.max_iterations))
+    nw = ctypes.c_int32()
+    k0 = ctypes.c_int64()
+    ms = (ctypes.c_double * 1)()
+    cap = 64
+    while True:
+        res = (_lib.WindowResult * cap)()
+        rc = ctx.lib.evd_solve_loaded_stream(ctx.h, tau, int(groups), p, res, cap,
+                                             ctypes.byref(nw), ctypes.byref(k0), ms)
+        if rc == _lib.EVD_ERR_ARG and nw.value > cap:
+            cap = nw.value
+            continue
+        if rc:
+            _raise(ctx, rc)
+        break
+    return _samples(res, nw.value, k0.value, tau, time.perf_counter() - start)
+
+
+def _samples(res, nw, k0, tau, wall):
+    solved = sum(1 for r in res[:nw] if r.status == _lib.EVD_OK)
     per = wall / max(solved, 1)
     samples = []
-    for w in range(nw.value):
+    for w in range(nw):
         r = res[w]
-        t_start = (k0_dev.value + w) * tau  # events.py:345
+        t_start = (k0 + w) * tau  # events.py:345
         if r.status == _lib.EVD_ERR_NO_EVENTS:
             continue
         if r.status == _lib.EVD_ERR_ITER_LIMIT:

@@ -18,6 +18,10 @@ Fixtures:
                 batches) and grid_search_oracle results
   synth.json    checksums of the reference simulator's windows for the
                 SURVEY §8(d) configurations (pins paper_2209_13168_b200.synth)
+  evd1.npz      EVD1 files (parse_event_bin, events.py:186-206): valid bodies
+                (sorted, unsorted with equal timestamps, large t_us) with the
+                reference's decoded arrays, and malformed / invalid bodies
+                with the reference's exception class and message
 """
 
 from __future__ import annotations
@@ -283,6 +287,67 @@ def make_bnb(big: bool):
         json.dump(out, fh, indent=1)
 
 
+# ------------------------------------------------------------------ evd1
+def make_evd1():
+    import struct
+    from eventdiv import events as ev
+    rng = np.random.default_rng(777)
+    rec = np.dtype([("t_us", "<u8"), ("x", "<f4"), ("y", "<f4"), ("p", "i1")])
+
+    def body(w, h, t_us, x, y, p, count=None):
+        r = np.empty(len(t_us), dtype=rec)
+        r["t_us"], r["x"], r["y"], r["p"] = t_us, x, y, p
+        n = len(t_us) if count is None else count
+        return struct.pack("<4sIIQ", b"EVD1", w, h, n) + r.tobytes()
+
+    cases = {}
+    n = 5000
+    t = np.sort(rng.integers(0, 3 * 10**6, n)).astype(np.uint64)
+    xs, ys = rng.uniform(0, 64, n), rng.uniform(0, 48, n)
+    ps = rng.choice([-1, 1], n).astype(np.int8)
+    cases["sorted"] = body(64, 48, t, xs, ys, ps)
+    tu = rng.integers(0, 2000, n).astype(np.uint64) * 1000  # many equal timestamps
+    cases["unsorted_ties"] = body(64, 48, tu, xs, ys, ps)
+    big = (np.uint64(2**60) + rng.integers(0, 2**40, 64).astype(np.uint64))
+    cases["large_t"] = body(64, 48, big, xs[:64], ys[:64], ps[:64])
+    cases["empty"] = body(8, 8, np.empty(0, np.uint64), [], [], [])
+    cases["edge_coords"] = body(4, 4, np.arange(4, dtype=np.uint64),
+                                np.array([0.0, 3.9999998, 0.0, 3.5], np.float32),
+                                np.array([0.0, 3.9999998, 3.9999998, 0.0], np.float32),
+                                np.array([1, -1, 1, -1], np.int8))
+    bad = {
+        "short_header": b"EVD1\0\0",
+        "bad_magic": b"NOPE" + b"\0" * 16,
+        "truncated": body(4, 4, np.arange(3, dtype=np.uint64), [1.0] * 3, [1.0] * 3, [1] * 3,
+                          count=5),
+        "out_of_frame": body(4, 4, np.arange(3, dtype=np.uint64), [1.0, 4.0, 1.0], [1.0] * 3,
+                             [1] * 3),
+        "negative_coord": body(4, 4, np.arange(2, dtype=np.uint64), [1.0, -0.5], [1.0] * 2,
+                               [1] * 2),
+        "nan_coord": body(4, 4, np.arange(2, dtype=np.uint64), [1.0, np.nan], [1.0] * 2, [1] * 2),
+        "bad_polarity": body(4, 4, np.arange(2, dtype=np.uint64), [1.0] * 2, [1.0] * 2, [1, 0]),
+        "zero_width": body(0, 4, np.arange(1, dtype=np.uint64), [0.0], [0.0], [1]),
+    }
+    out, meta = {}, {"valid": [], "invalid": {}}
+    for name, data in cases.items():
+        st = ev.parse_event_bin(data)
+        out[f"{name}_data"] = np.frombuffer(data, np.uint8)
+        for k in ("x", "y", "t"):
+            out[f"{name}_{k}"] = getattr(st, k)
+        out[f"{name}_p"] = st.polarity
+        out[f"{name}_geom"] = np.array([st.geometry.width, st.geometry.height])
+        meta["valid"].append(name)
+    for name, data in bad.items():
+        out[f"bad_{name}_data"] = np.frombuffer(data, np.uint8)
+        try:
+            ev.parse_event_bin(data)
+            meta["invalid"][name] = None
+        except Exception as exc:  # the reference's class and message
+            meta["invalid"][name] = [type(exc).__name__, str(exc)]
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(os.path.join(HERE, "evd1.npz"), **out)
+
+
 # ------------------------------------------------------------------ synth
 def make_synth():
     out = {}
@@ -299,12 +364,14 @@ def make_synth():
 
 if __name__ == "__main__":
     big = "--big" in sys.argv
-    what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["segments", "images", "bnb", "synth"]
+    what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["segments", "images", "bnb", "synth", "evd1"]
     if "segments" in what:
         make_segments()
     if "images" in what:
         make_images()
     if "synth" in what:
         make_synth()
+    if "evd1" in what:
+        make_evd1()
     if "bnb" in what:
         make_bnb(big)

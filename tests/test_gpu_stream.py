@@ -59,3 +59,55 @@ def test_stream_gaps_offset_start_and_iteration_limit():
         assert _key(dev) == _key(host)
     assert evd.stream_divergence(EventStream(np.empty(0), np.empty(0), np.empty(0),
                                              np.empty(0), s.geometry), evd.SolverParams()) == []
+
+
+# ------------------------------------------------------------------ EVD1 files
+def _evd1():
+    import json
+    import os
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "evd1.npz"))
+    return z, json.loads(bytes(z["meta"]).decode())
+
+
+def test_parse_event_bin_matches_reference():
+    z, meta = _evd1()
+    for name in meta["valid"]:
+        s = evd.parse_event_bin(z[f"{name}_data"].tobytes())
+        for k, attr in (("x", "x"), ("y", "y"), ("t", "t"), ("p", "polarity")):
+            assert np.array_equal(getattr(s, attr), z[f"{name}_{k}"]), (name, k)
+        assert [s.geometry.width, s.geometry.height] == z[f"{name}_geom"].tolist()
+    cls = {"EventFormatError": evd.EventFormatError,
+           "EventValidationError": evd.EventValidationError}
+    for name, (kind, msg) in meta["invalid"].items():
+        with pytest.raises(cls[kind]) as ei:
+            evd.parse_event_bin(z[f"bad_{name}_data"].tobytes())
+        assert str(ei.value) == msg, name
+
+
+def test_bin_unsorted_large_matches_oracle(rng):
+    """A shuffled 200k-record file: device radix sort == numpy stable argsort."""
+    import struct
+    n = 200_000
+    rec = np.dtype([("t_us", "<u8"), ("x", "<f4"), ("y", "<f4"), ("p", "i1")])
+    r = np.empty(n, dtype=rec)
+    r["t_us"] = rng.integers(0, 50_000, n)  # many ties
+    r["x"], r["y"] = rng.uniform(0, 240, n), rng.uniform(0, 180, n)
+    r["p"] = rng.choice([-1, 1], n)
+    data = struct.pack("<4sIIQ", b"EVD1", 240, 180, n) + r.tobytes()
+    x, y, t, p, _ = orc.parse_bin(data)
+    s = evd.parse_event_bin(data)
+    assert np.array_equal(s.x, x) and np.array_equal(s.y, y)
+    assert np.array_equal(s.t, t) and np.array_equal(s.polarity, p)
+
+
+def test_bin_to_samples_equals_host_pipeline(tmp_path):
+    s = _stream()
+    path = tmp_path / "s.bin"
+    evd.write_event_bin(s, path)
+    data = path.read_bytes()
+    params = evd.SolverParams()
+    host = evd.estimate_stream_divergence(evd.batch_stream(evd.parse_event_bin(data), 0.5),
+                                          params)
+    dev = evd.stream_divergence_bin(data, params)
+    assert len(dev) > 4 and _key(dev) == _key(host)

@@ -5,10 +5,13 @@ must reproduce every golden vector the reference generated
 (tests/golden/make_golden.py) bit for bit.
 """
 
+import json
+import os
+
 import numpy as np
 import pytest
 
-from conftest import f64, golden_segment_sets
+from conftest import GOLDEN, f64, golden_segment_sets
 from oracle import oracle as orc
 
 
@@ -90,3 +93,23 @@ def test_multithreaded_oracle_is_deterministic(img_golden):
     finally:
         orc.THREADS = 1
     assert np.array_equal(c1, c5) and f1 == f5
+
+
+def _evd1_golden():
+    z = np.load(os.path.join(GOLDEN, "evd1.npz"))
+    return z, json.loads(bytes(z["meta"]).decode())
+
+
+def test_evd1_oracle_matches_reference_parser():
+    z, meta = _evd1_golden()
+    for name in meta["valid"]:
+        x, y, t, p, geom = orc.parse_bin(z[f"{name}_data"].tobytes())
+        for k, v in (("x", x), ("y", y), ("t", t), ("p", p)):
+            assert np.array_equal(v, z[f"{name}_{k}"]), (name, k)
+            assert v.dtype == z[f"{name}_{k}"].dtype
+        assert list(geom) == z[f"{name}_geom"].tolist()
+    cls = {"EventFormatError": orc.FormatError, "EventValidationError": orc.ValidationError}
+    for name, (kind, msg) in meta["invalid"].items():
+        with pytest.raises(cls[kind]) as ei:
+            orc.parse_bin(z[f"bad_{name}_data"].tobytes())
+        assert str(ei.value) == msg
