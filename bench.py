@@ -182,6 +182,18 @@ def windows_line(ctx):
             "all_ok": all(r.status == 0 for r in res)}
 
 
+def stream_line():
+    """Whole-stream pipeline end to end (tools/bench_stream.py): 50 landing
+    descents at 240x180 as one stream and as one EVD1 file."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_stream.py"), "50"],
+                         capture_output=True, text=True, timeout=600)
+    try:
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return {"error": (out.stderr or out.stdout)[-300:]}
+
+
 def run_gpu(args, rank, world, local):
     import torch
     import paper_2209_13168_b200 as evd
@@ -309,6 +321,7 @@ def run_gpu(args, rank, world, local):
         if world == 1 and not args.no_extra:
             line["frontier_cfg3"] = frontier_line(ctx, stream)
             line["windows_cfg4"] = windows_line(ctx)
+            line["stream_e2e"] = stream_line()
         if world == 1 and not args.no_cpu:
             threads = host_threads()
             dt, r = cpu_solve_sample(batch, threads)

@@ -34,11 +34,30 @@ def main():
     t0 = time.perf_counter()
     host = evd.estimate_stream_divergence(evd.batch_stream(s, 0.5), params)
     t_host = time.perf_counter() - t0
-    same = [(a.t, a.divergence, a.contrast, a.iterations) for a in dev] == \
-           [(a.t, a.divergence, a.contrast, a.iterations) for a in host]
+    key = lambda ss: [(a.t, a.divergence, a.contrast, a.iterations) for a in ss]
+    # EVD1 file body -> samples, no host parse (t rounded to whole microseconds
+    # by the format, so these samples are for the file's stream)
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "s.bin")
+        evd.write_event_bin(s, path)
+        with open(path, "rb") as fh:
+            data = fh.read()
+    evd.stream_divergence_bin(data, params)  # warm
+    t0 = time.perf_counter()
+    binr = evd.stream_divergence_bin(data, params)
+    t_bin = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    hostb = evd.estimate_stream_divergence(evd.batch_stream(evd.parse_event_bin(data), 0.5),
+                                           params)
+    t_hostb = time.perf_counter() - t0
     print(json.dumps({"workload": f"stream: {d} descents 240x180, {s.n} events, {len(dev)} windows",
                       "stream_pipeline_s": t_dev, "windows_per_s": len(dev) / t_dev,
-                      "host_windowing_pipeline_s": t_host, "identical": same}), flush=True)
+                      "host_windowing_pipeline_s": t_host, "identical": key(dev) == key(host),
+                      "evd1_bytes": len(data), "evd1_pipeline_s": t_bin,
+                      "evd1_windows_per_s": len(binr) / t_bin,
+                      "evd1_parse_then_host_windowing_s": t_hostb,
+                      "evd1_identical": key(binr) == key(hostb)}), flush=True)
 
 
 if __name__ == "__main__":
