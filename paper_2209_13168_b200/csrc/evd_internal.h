@@ -43,7 +43,7 @@ struct SolveState {
     // per-node accumulators, double-buffered by node parity: 0 in_image,
     // 1 fully_inside A, 2 fully_inside B, 3 segment marks, 4 S_bar A, 5 S_bar B,
     // 6 exact-path events, 7 event work counter
-    unsigned long long acc[2][8];
+    alignas(16) unsigned long long acc[2][8];  // 16-byte aligned: vector loads
     // incumbent and diagnostics
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
@@ -85,7 +85,7 @@ struct SolveArgs {
 };
 
 constexpr int kBTraceIters = 128;
-constexpr int kBTraceSlots = 16;
+constexpr int kBTraceSlots = 20;
 constexpr int kBTraceMaxBlocks = 2048;
 
 constexpr long long kTraceIters = 1 << 14;

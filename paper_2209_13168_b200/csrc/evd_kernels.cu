@@ -12,6 +12,13 @@
 
 namespace evd {
 
+// Compiled only into the diagnostic build (EVD_TRACE_BUILD, libevd_trace.so):
+// the probes cost instruction-cache footprint in the per-node fixed phases.
+#ifdef EVD_TRACE_BUILD
+constexpr bool kTraceBuild = true;
+#else
+constexpr bool kTraceBuild = false;
+#endif
 constexpr int kThreads = 256;
 #ifndef EVD_SOLVE_THREADS
 #define EVD_SOLVE_THREADS 512
@@ -44,9 +51,16 @@ static int event_blocks(long long n)
     return b < 1 ? 1 : (int)b;
 }
 
+// Pixel increments are fire-and-forget L2 reductions.  The pointer reaches
+// the sampler through shared memory (WarpQueue::img), where the compiler can
+// no longer prove it global and emits a generic, value-returning ATOM; the
+// explicit red.global keeps every mark a RED.
 struct AtomicSink {
     unsigned int *img;
-    __device__ __forceinline__ void operator()(long long p) const { atomicAdd(img + p, 1u); }
+    __device__ __forceinline__ void operator()(long long p) const
+    {
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(img + p));
+    }
 };
 
 // Per-warp queue of built segments: lane l owns slots 2l, 2l+1.
@@ -359,16 +373,29 @@ template <class Q>
 __device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc,
                            const SolveArgs &dbg_a, long long dbg_it)
 {
+    if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 19);
     const int l0 = T.cut_leaf0[c], nl = T.cut_leaf0[c + 1] - l0;
     const int j = threadIdx.x & 7, ngroups = blockDim.x >> 3;
+    if (kTraceBuild && dbg_a.btrace) {
+        asm volatile("" ::"r"(nl));
+        bclock(dbg_a, dbg_it, 16);
+    }
     for (int i = threadIdx.x >> 3; i < nl; i += ngroups) {
         const int2 lf = T.leaves[l0 + i];
+        if (dbg_a.btrace && i == 0) {
+            asm volatile("" ::"r"(lf.x), "r"(lf.y));
+            bclock(dbg_a, dbg_it, 17);
+        }
         const double v = pairwise_leaf8(lf.x, lf.y, j, q);
+        if (dbg_a.btrace && i == 0) {
+            asm volatile("" ::"d"(v));
+            bclock(dbg_a, dbg_it, 18);
+        }
         if (j == 0) loc[i] = v;
     }
-    if (dbg_a.btrace) bclock(dbg_a, dbg_it, 14);
+    if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 14);
     __syncthreads();
-    if (dbg_a.btrace) bclock(dbg_a, dbg_it, 15);
+    if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 15);
     const int t0 = T.cut_trip0[c], ni = T.cut_trip0[c + 1] - t0;
     const int *lvl = T.cut_lvl + (long long)c * (kMaxLevels + 1);
     const int nlev = T.cut_nlev[c];
@@ -511,12 +538,14 @@ __device__ __forceinline__ long long globaltimer()
 // node evaluation i (0 = root) at 1 + kTraceSlots*i + slot, see TraceSlot.
 __device__ __forceinline__ void trace_point(const SolveArgs &a, long long it, int slot)
 {
+    if (!kTraceBuild) return;
     if (!a.trace || threadIdx.x != 0) return;
     if (slot < 0) a.trace[0] = globaltimer();
     else if (it < a.trace_iters) a.trace[1 + kTraceSlots * it + slot] = globaltimer();
 }
 __device__ __forceinline__ void trace_max(const SolveArgs &a, long long it, int slot)
 {
+    if (!kTraceBuild) return;
     if (!a.trace || threadIdx.x != 0 || it >= a.trace_iters) return;
     atomicMax(reinterpret_cast<unsigned long long *>(a.trace + 1 + kTraceSlots * it + slot),
               (unsigned long long)globaltimer());
@@ -524,12 +553,14 @@ __device__ __forceinline__ void trace_max(const SolveArgs &a, long long it, int 
 
 __device__ __forceinline__ void btrace_point(const SolveArgs &a, long long it, int k)
 {
+    if (!kTraceBuild) return;
     if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
     a.btrace[(it * a.group_blocks + blockIdx.x) * kBTraceSlots + k] = globaltimer();
 }
 // sub-phase markers (SM cycles) in slots 4.. of the block trace
 __device__ __forceinline__ void bclock(const SolveArgs &a, long long it, int k)
 {
+    if (!kTraceBuild) return;
     if (!a.btrace || threadIdx.x != 0 || it >= kBTraceIters) return;
     a.btrace[(it * a.group_blocks + blockIdx.x) * kBTraceSlots + k] = clock64();
 }
@@ -669,6 +700,7 @@ __device__ __forceinline__ FrontierEntry entry_load(const FrontierEntry *src)
 struct Replica {
     double lo, hi, c, den_lo, den_c, den_hi;  // node under evaluation
     double r_lo, r_c, r_hi;                   // RN(1 / den) for the filtered path
+    double mu;                                // point-image mean of the node (pixel phase)
     int mode, done, status, parity;
     double nu_hat, c_hat, bound_gap;
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
@@ -902,9 +934,17 @@ constexpr size_t kRegionA = kQueueBytes > kStepBytes ? kQueueBytes : kStepBytes;
 constexpr size_t kSolveSmemBytes = kRegionA + sizeof(TreeCache);
 
 template <bool FILTER>
-__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveArgs a)
+__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveArgs a_param)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+#ifdef EVD_ARGS_SMEM
+    __shared__ SolveArgs a_s;
+    if (threadIdx.x == 0) a_s = a_param;
+    __syncthreads();
+    const SolveArgs &a = a_s;
+#else
+    const SolveArgs &a = a_param;
+#endif
     // region A: warp queues (event phase) | cut scratch + frontier view (pixels, step)
     WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
     double *scratch = reinterpret_cast<double *>(smem);
@@ -915,7 +955,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
     const int GB = a.group_blocks;
     const int grp = blockIdx.x / GB, gb = blockIdx.x % GB;
     if (grp >= a.groups) return;
-    const bool tracer = grp == 0 && a.trace != nullptr;
+    const bool tracer = kTraceBuild && grp == 0 && a.trace != nullptr;
     unsigned long long *ctr = a.bar + 2 * grp;
     unsigned long long target = 0;
     SolveState *st = a.st + grp;
@@ -929,7 +969,16 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
     bool local_cuts;
     TreeDev gtree = a.tree;
     gtree.cutval = a.tree.cutval + (long long)grp * a.tree.C;
-    const TreeDev tree = cache_tree(gtree, tc, local_cuts, gb, GB);
+    // the plan's pointers live in shared memory: kept in registers they are
+    // spilled, and reloading them through L1 after an event phase cost
+    // several L2 round trips per node (measured ~4k cycles)
+    __shared__ TreeDev tree_s;
+    {
+        const TreeDev t = cache_tree(gtree, tc, local_cuts, gb, GB);
+        if (threadIdx.x == 0) tree_s = t;
+        __syncthreads();
+    }
+    const TreeDev &tree = tree_s;
     if (tracer && gb == 0) trace_point(a, 0, -1);
 
     for (int w = grp; w < a.n_windows; w += a.groups) {
@@ -1091,17 +1140,24 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
 
             // pixel phase: contrast subtrees of the point image, exact sums of
             // squares of both segment images; every image is left zeroed
+            // One thread per CTA reads the accumulators (all requests in flight
+            // together) and broadcasts mu through shared memory: 512 threads
+            // loading the same line after the barrier was measured ~4k cycles.
             if (threadIdx.x == 0) {
+                const ulonglong2 a01 = __ldcg(reinterpret_cast<const ulonglong2 *>(acc));
+                const unsigned long long a2 = __ldcg(acc + 2);
                 if (gb == 0) {
                     for (int k = 0; k < R.n_pending; k++) entry_store(fr + R.pend_idx[k], R.pend[k]);
                     unsigned long long *nxt = st->acc[par ^ 1];
                     for (int k = 0; k < 8; k++) __stcg(nxt + k, 0ull);
                 }
-                R.fiA = __ldcg(acc + 1);  // final after barrier 1; prefetch for the step
-                R.fiB = __ldcg(acc + 2);
+                R.fiA = a01.y;  // final after barrier 1; kept for the step
+                R.fiB = a2;
+                R.mu = ddiv((double)a01.x, (double)tree.M);
             }
             if (tr) bclock(a, it, 5);
-            const double mu = ddiv((double)__ldcg(acc), (double)tree.M);
+            __syncthreads();
+            const double mu = R.mu;
             if (tr) bclock(a, it, 13);
             for (int cut = gb, q = 0; cut < tree.C; cut += GB, q++) {
                 const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{P, mu}}, scratch,
@@ -1136,13 +1192,17 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             if (n0 <= kFrView)
                 for (long long i = threadIdx.x; i < n0; i += blockDim.x) view[i] = entry_load(fr + i);
             if (threadIdx.x == 0) {
-                R.sA = __ldcg(acc + 4);
-                R.sB = __ldcg(acc + 5);
-                R.marks += __ldcg(acc + 0) + __ldcg(acc + 3);
-                R.exact += __ldcg(acc + 6);
+                const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(acc + 2));
+                const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(acc + 4));
+                const ulonglong2 a67 = __ldcg(reinterpret_cast<const ulonglong2 *>(acc + 6));
+                const unsigned long long in_image = __ldcg(acc);
+                R.sA = a45.x;
+                R.sB = a45.y;
+                R.marks += in_image + a23.y;
+                R.exact += a67.x;
                 if (tr && gb == 0 && it < a.trace_iters) {  // per-node work counters
-                    a.trace[1 + kTraceSlots * it + kTrMarks] = (long long)__ldcg(acc + 3);
-                    a.trace[1 + kTraceSlots * it + kTrExact] = (long long)__ldcg(acc + 6);
+                    a.trace[1 + kTraceSlots * it + kTrMarks] = (long long)a23.y;
+                    a.trace[1 + kTraceSlots * it + kTrExact] = (long long)a67.x;
                 }
             }
             __syncthreads();

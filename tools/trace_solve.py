@@ -20,6 +20,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["EVD_TRACE"] = "1"  # read when the libevd context is created
+# the probes are compiled only into the diagnostic build
+os.environ.setdefault("EVD_LIB", os.path.join(ROOT, "paper_2209_13168_b200", "libevd_trace.so"))
 
 import paper_2209_13168_b200 as evd  # noqa: E402
 from paper_2209_13168_b200 import _lib, solver as sol, synth  # noqa: E402
@@ -82,7 +84,7 @@ if __name__ == "__main__":
 
 
 def block_trace(ctx, it_list=(40, 50, 80)):
-    S = 16
+    S = 20
     blocks = (_lib._i32 * 1)()
     buf = np.zeros(128 * 2048 * S, dtype=np.int64)
     ctx.lib.evd_solve_block_trace(ctx.h, _lib.ptr(buf, _lib._i64p), buf.size, blocks)
@@ -109,6 +111,11 @@ def block_trace(ctx, it_list=(40, 50, 80)):
         pre = e[:, 0] - raw[it, :, 5]
         print("   cut detail: mu=%.0f leaves=%.0f sync=%.0f" % (
             np.median(pre), np.median(e[:, 1] - e[:, 0]), np.median(e[:, 2] - e[:, 1])))
+        f = raw[it, :, 16:20].astype(np.float64)
+        print("   eval_cut entry after mu: %.0f cycles" % np.median(f[:, 3] - e[:, 0]))
+        print("   leaf detail (thread 0): cut_leaf0=%.0f leaves[]=%.0f leaf8=%.0f rest=%.0f" % (
+            np.median(f[:, 0] - e[:, 0]), np.median(f[:, 1] - f[:, 0]),
+            np.median(f[:, 2] - f[:, 1]), np.median(e[:, 1] - f[:, 2])))
 
 
 if "--blocks" in sys.argv:
