@@ -99,11 +99,24 @@ __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double
 
 // Out-of-line copy for the solve kernel, whose event loop calls it for both
 // child segments: one copy keeps the hot loop inside the instruction cache.
-__device__ __noinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
-                                             int H, WarpQueue &q, int slot, AtomicSink &sink,
-                                             int &marks)
+// Plain-value interface (image pointer in, chunks | marks << 16 out): a
+// reference to the caller's sink or mark counter would live in local memory.
+__device__ __noinline__ int segment_or_queue_ool(double ax, double ay, double bx, double by,
+                                                 int W, int H, WarpQueue &q, int slot,
+                                                 unsigned int *img)
 {
-    return segment_or_queue_inl<-1>(ax, ay, bx, by, W, H, q, slot, sink, marks);
+    AtomicSink sink{img};
+    int marks = 0;
+    const int c = segment_or_queue_inl<-1>(ax, ay, bx, by, W, H, q, slot, sink, marks);
+    return c | (marks << 16);  // chunks < 2^16 (W + H + 4 items / kChunk)
+}
+__device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
+                                                int H, WarpQueue &q, int slot,
+                                                const AtomicSink &sink, int &marks)
+{
+    const int r = segment_or_queue_ool(ax, ay, bx, by, W, H, q, slot, sink.img);
+    marks += r >> 16;
+    return r & 0xffff;
 }
 
 // Sample every chunk the warp queued, in rounds of 32: all lanes position
