@@ -310,6 +310,7 @@ struct Cursor {
     int iX, iY, eX, eY;   // next unconsumed item of each list; chunk ends
     double sX, sX2;       // values of X items iX, iX+1 (2 = none)
     double sY, sY2;
+    double kX, kY;        // grid coordinate of the item that enters each lookahead next
     double cur;           // item to mark next
     double after;         // first item after the chunk (for its last midpoint)
     Prev prev;
@@ -382,6 +383,9 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
     }
     c.sX2 = item_or_none(d.X, c.iX + 1, c.eX);
     c.sY2 = item_or_none(d.Y, c.iY + 1, c.eY);
+    // integers below 2^53, so the running k stays exact in binary64
+    c.kX = (double)(d.X.k0 + (long long)d.X.step * (c.iX + 2));
+    c.kY = (double)(d.Y.k0 + (long long)d.Y.step * (c.iY + 2));
     return true;
 }
 
@@ -409,19 +413,20 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
         nxt = tX ? c.sX : c.sY;
         const int idx = (tX ? c.iX : c.iY) + 2;  // the item that enters the lookahead
         const int lim = tX ? c.eX : c.eY;
-        const long long k = tX ? d.X.k0 + (long long)d.X.step * idx
-                               : d.Y.k0 + (long long)d.Y.step * idx;
-        double v = ddiv(dsub((double)k, tX ? cx0 : cy0), tX ? ddx : ddy);
+        const double k = tX ? c.kX : c.kY;
+        double v = ddiv(dsub(k, tX ? cx0 : cy0), tX ? ddx : ddy);
         v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
         if (idx >= lim) v = 2.0;
         if (tX) {
             c.iX++;
             c.sX = c.sX2;
             c.sX2 = v;
+            c.kX = dadd(c.kX, (double)d.X.step);
         } else {
             c.iY++;
             c.sY = c.sY2;
             c.sY2 = v;
+            c.kY = dadd(c.kY, (double)d.Y.step);
         }
     } else if (c.last) {
         nxt = 1.0;  // the trailing ts = 1

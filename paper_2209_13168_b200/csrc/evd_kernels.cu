@@ -154,8 +154,9 @@ __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int 
             sink.img = q.img[slot];
             active = cursor_init(q.d[slot], second ? r - q.na[L] : r, c);
         }
+        const SegDesc d = q.d[slot];  // in registers for the walk
         while (__any_sync(0xffffffffu, active))
-            if (active) active = cursor_step(q.d[slot], c, W, H, sink, marks);
+            if (active) active = cursor_step(d, c, W, H, sink, marks);
     }
     __syncwarp();
     return marks;
