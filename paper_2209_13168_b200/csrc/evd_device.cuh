@@ -220,16 +220,18 @@ struct CrossList {
 };
 
 // A clipped segment ready for sampling.  Its sample sequence is
-// [0, merge(X, Y), 1] (np.sort of the reference's ts array: both lists are
+// S = [0, merge(X, Y), 1] (np.sort of the reference's ts array: both lists are
 // monotone and clamped into [0, 1], so a two-way merge reproduces the sorted
-// multiset).  Long sequences are cut into `chunks` pieces by value: chunk j
-// holds the items with value in [j/J, (j+1)/J).  Crossings are uniformly
-// dense in the parameter, so the pieces hold nearly equal item counts, and
-// each piece finds its exact seams and its predecessor item with
-// CrossList::bound -- the marks equal one sequential pass.
+// multiset).  Long sequences are cut by position into chunks of `csize`
+// items: chunk j marks items [j*csize, (j+1)*csize) and the midpoint after
+// each of them.  A chunk finds its first item with a merge-path search (an
+// arithmetic estimate fixed up with exact item values) and recomputes its
+// predecessor and the midpoint call before it for dedup, so the marks equal one
+// sequential pass for any chunk size, and every chunk but a segment's last
+// holds exactly csize items (lanes of a warp sampling chunks stay in step).
 struct SegDesc {
     CrossList X, Y;  // X.c0 = cx0, X.dd = ddx, Y.c0 = cy0, Y.dd = ddy
-    int chunks;
+    int chunks, csize;
 };
 
 // Clip the closed segment a -> b (contrast.py:94-146).  Returns the number of
@@ -300,6 +302,7 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
     }
     const int items = 2 + d.X.n + d.Y.n;
     d.chunks = (items + C - 1) / C;
+    d.csize = C;
     return d.chunks;
 }
 
@@ -307,92 +310,105 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
 // to its successor (contrast.py:176-182).  Each list keeps its next two item
 // values, so the division that refills a list is off the critical path.
 struct Cursor {
-    int iX, iY, eX, eY;   // next unconsumed item of each list; chunk ends
+    int iX, iY;           // next unconsumed item of each list
+    int left;             // items of the chunk still to mark, cur included
+    int fin;              // cur is the trailing ts = 1
     double sX, sX2;       // values of X items iX, iX+1 (2 = none)
     double sY, sY2;
     double kX, kY;        // grid coordinate of the item that enters each lookahead next
     double cur;           // item to mark next
-    double after;         // first item after the chunk (for its last midpoint)
     Prev prev;
-    int last, fin;        // chunk ends with the trailing ts = 1; cur is that item
 };
 
-__device__ __forceinline__ double chunk_edge(int j, int J) { return (double)j / (double)J; }
-
-__device__ __forceinline__ double item_or_none(const CrossList &L, int i, int e)
+__device__ __forceinline__ double item_or_none(const CrossList &L, int i)
 {
-    return i < e ? L.at(i) : 2.0;
+    return i < L.n ? L.at(i) : 2.0;
 }
 
-// Position the cursor at chunk j of J; false if the chunk holds no item (its
-// neighbours then emit the midpoint across it).
+// Number of X items among the first p items of merge(X, Y) (X first on
+// equal values, as the walk takes them).  i is right iff X[i] does not come
+// before Y[p-i-1] and X[i-1] comes before Y[p-i]; the estimate from the
+// lists' arithmetic spacing is usually exact or one off.
+__device__ __forceinline__ int merge_split(const SegDesc &d, int p)
+{
+    const CrossList &X = d.X, &Y = d.Y;
+    const int lo = p - Y.n > 0 ? p - Y.n : 0, hi = p < X.n ? p : X.n;
+    const double ax = fabs(X.dd), ay = fabs(Y.dd);
+    const double ox = (X.c0 - (double)X.k0) * X.step, oy = (Y.c0 - (double)Y.k0) * Y.step;
+    const double v = (ax + ay > 0.0) ? ((double)p - ox - oy) / (ax + ay) : 0.0;
+    const double est = ceil(ox + v * ax);
+    int i = est < (double)lo ? lo : (est > (double)hi ? hi : (int)est);
+    // X[i] before Y[p-i-1]: then X[i] is among the first p (i too small)
+    auto too_small = [&](int k) { return k < X.n && p - k > 0 && X.at(k) <= Y.at(p - k - 1); };
+    while (i < hi && too_small(i)) i++;
+    while (i > lo && !too_small(i - 1)) i--;
+    return i;
+}
+
+// Position the cursor at chunk j (items [j*csize, (j+1)*csize) of S).
 __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
 {
-    const int J = d.chunks;
-    c.last = j == J - 1;
+    const CrossList &X = d.X, &Y = d.Y;
+    const int T = X.n + Y.n, N = T + 2, m0 = j * d.csize;
+    if (m0 >= N) return false;
+    c.left = N - m0 < d.csize ? N - m0 : d.csize;
     c.fin = 0;
-    c.prev = Prev{1, 0, 1, 0};
-    if (!c.last) {
-        double b, aX, aY;
-        const double vb = chunk_edge(j + 1, J);
-        c.eX = d.X.bound(vb, b, aX);
-        c.eY = d.Y.bound(vb, b, aY);
-        c.after = aX < aY ? aX : aY;
-        if (c.after >= 2.0) c.after = 1.0;  // no item >= vb: the trailing ts = 1 follows
-    } else {
-        c.eX = d.X.n;
-        c.eY = d.Y.n;
-        c.after = 2.0;
-    }
-    if (j == 0) {  // the leading ts = 0 starts the first chunk
+    if (m0 == 0) {  // the leading ts = 0 starts the first chunk
         c.iX = 0;
         c.iY = 0;
         c.cur = 0.0;
-        c.sX = item_or_none(d.X, 0, c.eX);
-        c.sY = item_or_none(d.Y, 0, c.eY);
+        c.prev = Prev{1, 0, 1, 0};
+        c.sX = item_or_none(X, 0);
+        c.sX2 = item_or_none(X, 1);
+        c.sY = item_or_none(Y, 0);
+        c.sY2 = item_or_none(Y, 1);
     } else {
-        double pX, fX, pY, fY;
-        const double va = chunk_edge(j, J);
-        c.iX = d.X.bound(va, pX, fX);
-        c.iY = d.Y.bound(va, pY, fY);
-        if (c.iX >= c.eX) fX = 2.0;
-        if (c.iY >= c.eY) fY = 2.0;
+        const int p = m0 - 1;  // S[m0] = merged[p], or the trailing 1 when p == T
+        const int i = p < T ? merge_split(d, p) : X.n, jy = p - i;
+        const double xp = i > 0 ? X.at(i - 1) : -1.0, yp = jy > 0 ? Y.at(jy - 1) : -1.0;
         double first;
-        if (fX < 2.0 && fX <= fY) {
-            first = fX;
-            c.iX++;
-            fX = item_or_none(d.X, c.iX, c.eX);
-        } else if (fY < 2.0) {
-            first = fY;
-            c.iY++;
-            fY = item_or_none(d.Y, c.iY, c.eY);
-        } else if (c.last) {
-            first = 1.0;  // only the trailing ts = 1 remains
+        if (p >= T) {
+            first = 1.0;
             c.fin = 1;
+            c.iX = X.n;
+            c.iY = Y.n;
+            c.sX = c.sX2 = c.sY = c.sY2 = 2.0;
         } else {
-            return false;
+            const double xi = item_or_none(X, i), yj = item_or_none(Y, jy);
+            if (xi <= yj) {  // X first on equal values
+                first = xi;
+                c.iX = i + 1;
+                c.iY = jy;
+                c.sX = item_or_none(X, i + 1);
+                c.sX2 = item_or_none(X, i + 2);
+                c.sY = yj;
+                c.sY2 = item_or_none(Y, jy + 1);
+            } else {
+                first = yj;
+                c.iX = i;
+                c.iY = jy + 1;
+                c.sX = xi;
+                c.sX2 = item_or_none(X, i + 1);
+                c.sY = item_or_none(Y, jy + 1);
+                c.sY2 = item_or_none(Y, jy + 2);
+            }
         }
-        // predecessor: the largest item < va, or the leading ts = 0
-        double p = pX > pY ? pX : pY;
-        if (p < 0.0) p = 0.0;
-        const double sm = dmul(0.5, dadd(p, first));
-        c.prev = point_range(dadd(d.X.c0, dmul(sm, d.X.dd)), dadd(d.Y.c0, dmul(sm, d.Y.dd)));
+        // predecessor: the largest earlier item, or the leading ts = 0
+        double pr = xp > yp ? xp : yp;
+        if (pr < 0.0) pr = 0.0;
+        const double sm = dmul(0.5, dadd(pr, first));
+        c.prev = point_range(dadd(X.c0, dmul(sm, X.dd)), dadd(Y.c0, dmul(sm, Y.dd)));
         c.cur = first;
-        c.sX = fX;
-        c.sY = fY;
     }
-    c.sX2 = item_or_none(d.X, c.iX + 1, c.eX);
-    c.sY2 = item_or_none(d.Y, c.iY + 1, c.eY);
     // integers below 2^53, so the running k stays exact in binary64
-    c.kX = (double)(d.X.k0 + (long long)d.X.step * (c.iX + 2));
-    c.kY = (double)(d.Y.k0 + (long long)d.Y.step * (c.iY + 2));
+    c.kX = (double)(X.k0 + (long long)X.step * (c.iX + 2));
+    c.kY = (double)(Y.k0 + (long long)Y.step * (c.iY + 2));
     return true;
 }
 
-// One item: mark it, advance to its successor (the list it comes from shifts
-// its lookahead and refills it with one division on selected operands, so
-// lanes stay converged), mark the midpoint.  Returns false once the chunk is
-// finished.
+// One item: mark it, find its successor (the list it comes from shifts its
+// lookahead and refills it with one division on selected operands, so lanes
+// stay converged), mark the midpoint.  Returns false once the chunk is done.
 #ifdef EVD_OUTLINE_STEP
 #define EVD_STEP_INLINE __noinline__
 #else
@@ -405,14 +421,14 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
     const double cx0 = d.X.c0, ddx = d.X.dd, cy0 = d.Y.c0, ddy = d.Y.dd;
     marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H, c.prev,
                         sink);
-    if (c.fin) return false;
+    if (c.fin) return false;  // the trailing ts = 1 has no successor
     const bool tX = c.sX < 2.0 && c.sX <= c.sY;
     const bool tY = !tX && c.sY < 2.0;
-    double nxt;
+    double nxt = 1.0;  // the trailing ts = 1 when both lists are spent
     if (tX || tY) {
         nxt = tX ? c.sX : c.sY;
         const int idx = (tX ? c.iX : c.iY) + 2;  // the item that enters the lookahead
-        const int lim = tX ? c.eX : c.eY;
+        const int lim = tX ? d.X.n : d.Y.n;
         const double k = tX ? c.kX : c.kY;
         double v = ddiv(dsub(k, tX ? cx0 : cy0), tX ? ddx : ddy);
         v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
@@ -428,19 +444,13 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
             c.sY2 = v;
             c.kY = dadd(c.kY, (double)d.Y.step);
         }
-    } else if (c.last) {
-        nxt = 1.0;  // the trailing ts = 1
-        c.fin = 1;
     } else {
-        const double sm = dmul(0.5, dadd(c.cur, c.after));  // midpoint into the next chunk
-        marks += mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev,
-                            sink);
-        return false;
+        c.fin = 1;
     }
     const double sm = dmul(0.5, dadd(c.cur, nxt));
     marks += mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
     c.cur = nxt;
-    return true;
+    return --c.left > 0;
 }
 
 // Sample chunk j of a built segment to the end.
