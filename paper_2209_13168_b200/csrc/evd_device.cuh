@@ -193,30 +193,6 @@ struct CrossList {
         else if (s > 1.0) s = 1.0;
         return s;
     }
-    // Index i of the first item >= v (items [0, i) are < v), found from an
-    // arithmetic estimate fixed up with exact item values; also returns the
-    // values of item i-1 (`below`, -1 if none) and item i (`above`, 2 if none).
-    __device__ int bound(double v, double &below, double &above) const
-    {
-        const double kv = dadd(c0, dmul(v, dd));
-        const double est = step > 0 ? ceil(kv - (double)k0) : ceil((double)k0 - kv);
-        int i = est < 0.0 ? 0 : (est > (double)n ? n : (int)est);
-        double lo = i > 0 ? at(i - 1) : -1.0;
-        double hi = i < n ? at(i) : 2.0;
-        while (i > 0 && lo >= v) {
-            i--;
-            hi = lo;
-            lo = i > 0 ? at(i - 1) : -1.0;
-        }
-        while (i < n && hi < v) {
-            i++;
-            lo = hi;
-            hi = i < n ? at(i) : 2.0;
-        }
-        below = lo;
-        above = hi;
-        return i;
-    }
 };
 
 // A clipped segment ready for sampling.  Its sample sequence is

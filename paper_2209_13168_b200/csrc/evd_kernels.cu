@@ -26,7 +26,7 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #ifndef EVD_CHUNK
-#define EVD_CHUNK 32
+#define EVD_CHUNK 16
 #endif
 constexpr int kChunk = EVD_CHUNK;  // sample items per supercover chunk
 constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
