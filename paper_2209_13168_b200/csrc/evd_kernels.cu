@@ -28,7 +28,11 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #ifndef EVD_CHUNK
 #define EVD_CHUNK 16
 #endif
-constexpr int kChunk = EVD_CHUNK;  // sample items per supercover chunk
+constexpr int kChunk = EVD_CHUNK;
+#ifndef EVD_GUIDED_WIDTH
+#define EVD_GUIDED_WIDTH (1.0 / 16)
+#endif
+constexpr double kGuidedWidth = EVD_GUIDED_WIDTH;  // nodes wider than this claim guided batches  // sample items per supercover chunk
 constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
 
 static int g_num_sms = 0;
@@ -613,6 +617,7 @@ struct EventJob {
     unsigned long long *acc;
     long long gsz;
     int gb;
+    int guided;  // shrink claims as the counter runs out (wide nodes)
 };
 
 __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &wq,
@@ -625,15 +630,21 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
     unsigned int *P = j.P;
     unsigned long long *acc = j.acc;
     AtomicSink sa{j.A}, sb{j.B};
-    // One static batch of 32 events per warp, then batches of 32 from the
-    // node's work counter.  The pass is latency-bound (a few batches per warp
-    // at narrow nodes), so claiming several batches at once was measured
-    // slower (tools/probe_events.py): it serialises them on fewer warps.
+    // One static batch of 32 events per warp, then batches from the node's
+    // work counter.  Narrow nodes take batches of 32 (the pass is latency-
+    // bound, a few batches per warp; claiming more at once was measured
+    // slower, tools/probe_events.py).  Wide nodes, where one batch can hold
+    // tens of microseconds of sampling, shrink their claims as the counter
+    // runs out (guided self-scheduling, down to 4 events) so the warps finish
+    // together; the sampler still spreads a small batch's chunks over all
+    // 32 lanes.
+    const long long warps = gsz >> 5;
     long long base = j.gb * (long long)blockDim.x + (threadIdx.x & ~31);
+    int size = 32;
     while (base < n) {
         const long long i = base + lane;
         int cA = 0, cB = 0, dummy = 0;
-        if (i < n) {
+        if (lane < size && i < n) {
             const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
             const Warped wl = warp_event(x, y, t, j.lo, j.den_lo, j.cx, j.cy);
             const Warped wc = warp_event(x, y, t, j.c, j.den_c, j.cx, j.cy);
@@ -656,8 +667,14 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
         }
         if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain(wq, cA, cB, W, H);
         v[3] += dummy;
+        if (j.guided) {
+            // claim size from the remaining events as last seen by this warp
+            const long long rem = n - base;
+            long long s = rem / (2 * warps);
+            size = (int)(s < 4 ? 4 : (s > 32 ? 32 : s));
+        }
         long long nb = 0;
-        if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, 32ull);
+        if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, (unsigned long long)size);
         base = __shfl_sync(0xffffffffu, nb, 0);
     }
 }
@@ -1058,7 +1075,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             // both give the same images
             if (!FILTER || dsub(hi, lo) > kFilterWidth) {
                 EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
-                           W, H, P, A, B, mode, acc, gsz, gb};
+                           W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth};
                 event_pass_exact(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
@@ -1401,7 +1418,7 @@ cudaError_t launch_event_probe(const double *xc, const double *yc, const double 
     set_attrs();
     EventJob j{xc, yc, t, n, nu3[0], nu3[1], nu3[2], den3[0], den3[1], den3[2], cx, cy, W, H,
                nullptr, nullptr, nullptr, kModeNode, nullptr,
-               (long long)blocks * kSolveThreads, 0};
+               (long long)blocks * kSolveThreads, 0, 1};
     k_event_probe<<<blocks, kSolveThreads, kQueueBytes, s>>>(j, reps, ctrs, span, scratch,
                                                              (long long)W * H);
     return cudaGetLastError();

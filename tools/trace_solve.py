@@ -119,4 +119,5 @@ def block_trace(ctx, it_list=(40, 50, 80)):
 
 
 if "--blocks" in sys.argv:
-    block_trace(_lib.context())
+    its = [int(x) for a in sys.argv if a.startswith("--nodes=") for x in a.split("=")[1].split(",")]
+    block_trace(_lib.context(), *([its] if its else []))
