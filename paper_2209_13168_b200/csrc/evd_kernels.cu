@@ -28,6 +28,9 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #ifndef EVD_CHUNK
 #define EVD_CHUNK 16
 #endif
+#ifndef EVD_FRONT_INLINE
+#define EVD_FRONT_INLINE 6
+#endif
 constexpr int kChunk = EVD_CHUNK;
 #ifndef EVD_GUIDED_WIDTH
 #define EVD_GUIDED_WIDTH (1.0 / 16)
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
         int c = 0, m = 0;
         if (valid) {
             fi += fully_inside(a.x, a.y, b.x, b.y, W, H);
-            c = segment_or_queue_inl<6>(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
+            c = segment_or_queue_inl<EVD_FRONT_INLINE>(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
         }
         if (__any_sync(0xffffffffu, c != 0)) warp_drain(wq, c, 0, W, H);
     }
