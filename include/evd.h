@@ -182,6 +182,22 @@ int evd_solve_loaded_stream(evd_ctx *ctx, double tau, int32_t groups,
  * resident for evd_solve_loaded_stream / evd_stream_copy. */
 int evd_load_bin(evd_ctx *ctx, const uint8_t *data, int64_t size, int32_t *width,
                  int32_t *height, int64_t *n);
+/* Upload a host stream (time-sorted, validated as EventStream is) as the
+ * resident stream; p (polarity) may be NULL. */
+int evd_load_stream(evd_ctx *ctx, const double *x, const double *y, const double *t,
+                    const int8_t *p, int64_t n, int32_t width, int32_t height);
+
+/* ---- preprocessing of the resident stream ----------- */
+/* pixel_counts (events.py:273-281): floor-binned per-pixel counts, H*W int64. */
+int evd_pixel_counts(evd_ctx *ctx, int64_t *counts);
+/* remove_hot_pixels (events.py:284-300): median and MAD of the nonzero counts
+ * (device sorts; numpy's median of an even count = mean of the middle two),
+ * threshold = med + k*mad, events on pixels above it dropped (stable).
+ * *n = events kept; *threshold = the threshold (0 for an empty stream). */
+int evd_stream_remove_hot_pixels(evd_ctx *ctx, double k, int64_t *n, double *threshold);
+/* rescale_events (events.py:303-313): x * (W'/W), y * (H'/H), capped below W', H'. */
+int evd_stream_rescale(evd_ctx *ctx, int32_t width, int32_t height);
+
 /* Copy the resident stream to host arrays of n elements (any may be NULL). */
 int evd_stream_copy(evd_ctx *ctx, double *x, double *y, double *t, int8_t *p);
 

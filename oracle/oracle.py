@@ -267,3 +267,34 @@ def parse_bin(data: bytes):
         if not np.isin(p, (-1, 1)).all():
             raise ValidationError("polarity must be +1 or -1")
     return x, y, t, p, (int(width), int(height))
+
+
+# ------------------------------------------------------------------ preprocessing
+def pixel_counts(x, y, width, height):
+    """events.py:273-281 restated."""
+    counts = np.zeros((height, width), dtype=np.int64)
+    if len(x):
+        np.add.at(counts, (np.floor(y).astype(np.intp), np.floor(x).astype(np.intp)), 1)
+    return counts
+
+
+def remove_hot_pixels(x, y, t, p, width, height, k=10.0):
+    """events.py:284-300 restated: returns (x, y, t, p, threshold)."""
+    if k <= 0:
+        raise ValueError("k must be positive")
+    if len(x) == 0:
+        return x, y, t, p, 0.0
+    counts = pixel_counts(x, y, width, height)
+    nz = counts[counts > 0].astype(np.float64)
+    med = np.median(nz)
+    mad = np.median(np.abs(nz - med))
+    threshold = med + k * mad
+    keep = ~(counts > threshold)[np.floor(y).astype(np.intp), np.floor(x).astype(np.intp)]
+    return x[keep], y[keep], t[keep], p[keep], float(threshold)
+
+
+def rescale(x, y, width, height, width2, height2):
+    """events.py:303-313 restated: returns (x, y)."""
+    sx, sy = width2 / width, height2 / height
+    return (np.minimum(x * sx, np.nextafter(float(width2), 0.0)),
+            np.minimum(y * sy, np.nextafter(float(height2), 0.0)))

@@ -10,7 +10,8 @@ from .contrast import (ContrastBound, EventImage, accumulate_image, bound_terms,
                        image_contrast, image_contrast_expanded, rasterize_segment,
                        upper_bound_image)
 from .events import (BIN_MAGIC, EventBatch, EventFormatError, EventStream, EventValidationError,
-                     SensorGeometry, batch_stream, parse_event_bin, write_event_bin)
+                     SensorGeometry, batch_stream, parse_event_bin, pixel_counts,
+                     remove_hot_pixels, rescale_events, write_event_bin)
 from .geometry import (CheiralityError, DivergenceSample, VelocityInterval,
                        continuous_divergence, divergence_from_velocity, radial_warp,
                        velocity_domain, warp_batch, warp_scale)

@@ -28,7 +28,8 @@ SYMBOLS = (
     "evd_rasterize_segments",
     "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
     "evd_probe_events", "evd_solve_stream", "evd_solve_loaded_stream", "evd_load_bin",
-    "evd_stream_copy",
+    "evd_stream_copy", "evd_load_stream", "evd_pixel_counts", "evd_stream_remove_hot_pixels",
+    "evd_stream_rescale",
     "evd_pow2_table",
 )
 
@@ -106,6 +107,11 @@ _SIGS = {
     "evd_load_bin": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64, ctypes.POINTER(_i32),
                                     ctypes.POINTER(_i32), _i64p]),
     "evd_stream_copy": (ctypes.c_int, [_vp, _d, _d, _d, ctypes.POINTER(ctypes.c_int8)]),
+    "evd_load_stream": (ctypes.c_int, [_vp, _d, _d, _d, ctypes.POINTER(ctypes.c_int8), _i64, _i32,
+                                       _i32]),
+    "evd_pixel_counts": (ctypes.c_int, [_vp, _i64p]),
+    "evd_stream_remove_hot_pixels": (ctypes.c_int, [_vp, _f64, _i64p, _d]),
+    "evd_stream_rescale": (ctypes.c_int, [_vp, _i32, _i32]),
     "evd_pow2_table": (ctypes.c_int, [_i64, _i64, _d]),
 }
 

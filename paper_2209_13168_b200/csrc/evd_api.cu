@@ -100,6 +100,7 @@ struct evd_ctx {
     DevBuf<signed char> sp;           // its polarity (evd_load_bin)
     DevBuf<unsigned char> sbytes, sscratch;  // EVD1 body, decode scratch
     DevBuf<unsigned int> sflags;
+    DevBuf<unsigned int> pcounts;        // evd_pixel_counts
     long long sn = -1;                // resident stream length (-1: none)
     int sW = 0, sH = 0;
     bool s_has_p = false;
@@ -447,6 +448,7 @@ void evd_destroy(evd_ctx *ctx)
     ctx->sbytes.release();
     ctx->sscratch.release();
     ctx->sflags.release();
+    ctx->pcounts.release();
     TreePlan &tp = ctx->tree;
     tp.leaves.release();
     tp.cut_leaf0.release();
@@ -1158,6 +1160,97 @@ int evd_load_bin(evd_ctx *ctx, const uint8_t *data, int64_t size, int32_t *width
     *width = (int32_t)w;
     *height = (int32_t)h;
     *n_out = n;
+    return EVD_OK;
+}
+
+int evd_load_stream(evd_ctx *ctx, const double *x, const double *y, const double *t,
+                    const int8_t *p, int64_t n, int32_t width, int32_t height)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (n < 0 || width < 1 || height < 1 || (n > 0 && (!x || !y || !t)))
+        return fail(ctx, EVD_ERR_ARG, "bad evd_load_stream arguments");
+    CU(cudaSetDevice(ctx->device));
+    const long long m = std::max<long long>(n, 1);
+    CU(ctx->sx.ensure(m));
+    CU(ctx->sy.ensure(m));
+    CU(ctx->st.ensure(m));
+    CU(ctx->sp.ensure(m));
+    if (n > 0) {
+        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (p) CU(cudaMemcpyAsync(ctx->sp.p, p, n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->sn = n;
+    ctx->sW = width;
+    ctx->sH = height;
+    ctx->s_has_p = p != nullptr;
+    return EVD_OK;
+}
+
+int evd_pixel_counts(evd_ctx *ctx, int64_t *counts)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (ctx->sn < 0) return fail(ctx, EVD_ERR_STATE, "no stream loaded");
+    if (!counts) return fail(ctx, EVD_ERR_ARG, "counts is NULL");
+    CU(cudaSetDevice(ctx->device));
+    const long long M = (long long)ctx->sW * ctx->sH;
+    CU(ctx->pcounts.ensure(M));
+    int launches = 0;
+    CU(pixel_counts_dev(ctx->sx.p, ctx->sy.p, ctx->sn, ctx->sW, ctx->sH, ctx->pcounts.p, &launches,
+                        ctx->stream));
+    ctx->launches += launches;
+    std::vector<unsigned int> h(M);
+    CU(cudaMemcpyAsync(h.data(), ctx->pcounts.p, M * sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (long long i = 0; i < M; i++) counts[i] = h[i];
+    return EVD_OK;
+}
+
+int evd_stream_remove_hot_pixels(evd_ctx *ctx, double k, int64_t *n_out, double *threshold)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!(k > 0.0)) return fail(ctx, EVD_ERR_ARG, "k must be positive");  // events.py:286-287
+    if (ctx->sn < 0) return fail(ctx, EVD_ERR_STATE, "no stream loaded");
+    if (!ctx->s_has_p) return fail(ctx, EVD_ERR_STATE, "the loaded stream has no polarity");
+    if (n_out) *n_out = ctx->sn;
+    if (threshold) *threshold = 0.0;
+    if (ctx->sn == 0) return EVD_OK;  // events.py:288-289
+    CU(cudaSetDevice(ctx->device));
+    const long long n = ctx->sn, M = (long long)ctx->sW * ctx->sH;
+    const size_t bytes = preprocess_scratch_bytes(n, M);
+    CU(ctx->sscratch.ensure(bytes));
+    long long kept = 0;
+    double thr = 0.0;
+    int launches = 0;
+    cudaError_t e = remove_hot_pixels_dev(ctx->sx.p, ctx->sy.p, ctx->st.p, ctx->sp.p, n, ctx->sW,
+                                          ctx->sH, k, ctx->sscratch.p, ctx->sscratch.cap, &kept,
+                                          &thr, &launches, ctx->stream);
+    ctx->launches += launches;
+    if (e != cudaSuccess) return fail(ctx, EVD_ERR_CUDA, "remove_hot_pixels: %s", cudaGetErrorString(e));
+    ctx->sn = kept;
+    if (n_out) *n_out = kept;
+    if (threshold) *threshold = thr;
+    return EVD_OK;
+}
+
+int evd_stream_rescale(evd_ctx *ctx, int32_t width, int32_t height)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (width < 1 || height < 1)
+        return fail(ctx, EVD_ERR_VALIDATION, "sensor dimensions must be positive, got %dx%d", width,
+                    height);
+    if (ctx->sn < 0) return fail(ctx, EVD_ERR_STATE, "no stream loaded");
+    CU(cudaSetDevice(ctx->device));
+    // events.py:305-312
+    const double sx = (double)width / (double)ctx->sW, sy = (double)height / (double)ctx->sH;
+    const double xmax = std::nextafter((double)width, 0.0), ymax = std::nextafter((double)height, 0.0);
+    int launches = 0;
+    CU(rescale_dev(ctx->sx.p, ctx->sy.p, ctx->sn, sx, sy, xmax, ymax, &launches, ctx->stream));
+    ctx->launches += launches;
+    ctx->sW = width;
+    ctx->sH = height;
     return EVD_OK;
 }
 

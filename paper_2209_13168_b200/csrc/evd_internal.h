@@ -144,6 +144,15 @@ cudaError_t decode_bin(const unsigned char *body_dev, long long n, int W, int H,
                        unsigned int *flags_dev, unsigned int *flags_host, int *launches,
                        cudaStream_t s);
 size_t decode_scratch_bytes(long long n);
+cudaError_t pixel_counts_dev(const double *x, const double *y, long long n, int W, int H,
+                             unsigned int *counts, int *launches, cudaStream_t s);
+cudaError_t remove_hot_pixels_dev(double *x, double *y, double *t, signed char *p, long long n,
+                                  int W, int H, double k, void *scratch, size_t scratch_bytes,
+                                  long long *n_out, double *threshold_out, int *launches,
+                                  cudaStream_t s);
+size_t preprocess_scratch_bytes(long long n, long long M);
+cudaError_t rescale_dev(double *x, double *y, long long n, double sx, double sy, double xmax,
+                        double ymax, int *launches, cudaStream_t s);
 void launch_window_bounds(const double *t, long long n, long long k0, int nw, double tau,
                           long long *lo, long long *hi, cudaStream_t s);
 void launch_gather_windows(const double *x, const double *y, const double *t,

@@ -11,8 +11,11 @@ pass them unchanged (every entry point in this package duck-types on the fields
 * ``parse_event_bin`` -- ``pkg/src/eventdiv/events.py:186-206`` (EVD1 decoded on the
   device); ``write_event_bin`` (``:236-246``) for round trips
 
-CSV parsing, hot-pixel removal, rescaling and subsampling are outside the hot
-path (SURVEY §2 row 5) and are not provided here.
+* ``pixel_counts`` / ``remove_hot_pixels`` / ``rescale_events`` -- ``events.py:273-313``
+  on the device
+
+CSV parsing and subsampling (numpy PCG64 stream parity) stay outside the hot
+path (SURVEY §2 row 5, §8(f) row 4) and are not provided here.
 """
 
 from __future__ import annotations
@@ -191,3 +194,75 @@ def write_event_bin(stream: EventStream, path) -> None:
     with open(Path(path), "wb") as fh:
         fh.write(struct.pack("<4sIIQ", BIN_MAGIC, g.width, g.height, stream.n))
         fh.write(body.tobytes())
+
+
+def _stream_ctx(stream, ctx=None):
+    """Upload ``stream`` as the context's resident stream (evd_load_stream)."""
+    import ctypes
+
+    from . import _lib
+    ctx = ctx or _lib.context()
+    x, y, t = _lib.f64(stream.x), _lib.f64(stream.y), _lib.f64(stream.t)
+    p = np.ascontiguousarray(stream.polarity, dtype=np.int8)
+    g = stream.geometry
+    rc = ctx.lib.evd_load_stream(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t),
+                                 p.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), len(t),
+                                 g.width, g.height)
+    if rc:
+        raise _lib.EvdError(rc, ctx.error_text())
+    return ctx
+
+
+def _resident_stream(ctx, n: int, geometry: SensorGeometry) -> EventStream:
+    import ctypes
+
+    from . import _lib
+    x, y, t = (np.empty(n, dtype=np.float64) for _ in range(3))
+    p = np.empty(n, dtype=np.int8)
+    if n:
+        rc = ctx.lib.evd_stream_copy(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t),
+                                     p.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+        if rc:
+            raise _lib.EvdError(rc, ctx.error_text())
+    return EventStream(x, y, t, p, geometry)
+
+
+def pixel_counts(stream: EventStream, ctx=None) -> np.ndarray:
+    """Per-pixel event counts (height x width), floor-binned (``events.py:273-281``)."""
+    from . import _lib
+    ctx = _stream_ctx(stream, ctx)
+    g = stream.geometry
+    counts = np.empty((g.height, g.width), dtype=np.int64)
+    rc = ctx.lib.evd_pixel_counts(ctx.h, _lib.ptr(counts, _lib._i64p))
+    if rc:
+        raise _lib.EvdError(rc, ctx.error_text())
+    return counts
+
+
+def remove_hot_pixels(stream: EventStream, k: float = 10.0, ctx=None) -> EventStream:
+    """Drop all events on pixels whose count exceeds median + k*MAD of the
+    nonzero counts (``events.py:284-300``), on the device."""
+    import ctypes
+
+    from . import _lib
+    if k <= 0:
+        raise ValueError("k must be positive")
+    if stream.n == 0:
+        return stream
+    ctx = _stream_ctx(stream, ctx)
+    n = ctypes.c_int64()
+    thr = ctypes.c_double()
+    rc = ctx.lib.evd_stream_remove_hot_pixels(ctx.h, float(k), ctypes.byref(n), ctypes.byref(thr))
+    if rc:
+        raise _lib.EvdError(rc, ctx.error_text())
+    return _resident_stream(ctx, n.value, stream.geometry)
+
+
+def rescale_events(stream: EventStream, target: SensorGeometry, ctx=None) -> EventStream:
+    """Scale event coordinates onto a new sensor grid (``events.py:303-313``)."""
+    from . import _lib
+    ctx = _stream_ctx(stream, ctx)
+    rc = ctx.lib.evd_stream_rescale(ctx.h, target.width, target.height)
+    if rc:
+        raise _lib.EvdError(rc, ctx.error_text())
+    return _resident_stream(ctx, stream.n, target)

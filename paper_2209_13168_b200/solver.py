@@ -250,18 +250,35 @@ def stream_divergence(stream, params: SolverParams, tau: float | None = None, gr
 
 
 def stream_divergence_bin(data: bytes, params: SolverParams, tau: float | None = None,
-                          groups: int = 0, ctx=None) -> list[DivergenceSample]:
+                          groups: int = 0, hot_pixel_k: float | None = None,
+                          rescale_to=None, ctx=None) -> list[DivergenceSample]:
     """EVD1 file body -> divergence samples without a host parse: the records
-    are decoded on the device (evd_load_bin) and the resident stream is
-    windowed and solved there (evd_solve_loaded_stream).  Equals
-    ``estimate_stream_divergence(batch_stream(parse_event_bin(data), tau), params)``."""
+    are decoded on the device (evd_load_bin), optionally cleaned of hot pixels
+    (``hot_pixel_k``) and rescaled (``rescale_to``, a SensorGeometry) in place,
+    and the resident stream is windowed and solved there
+    (evd_solve_loaded_stream).  Equals ``estimate_stream_divergence(
+    batch_stream(rescale_events(remove_hot_pixels(parse_event_bin(data), k),
+    target), tau), params)``."""
     from .events import load_bin_resident
     tau = float(params.tau if tau is None else tau)
     if tau <= 0:
         raise ValueError("tau must be positive")
+    if hot_pixel_k is not None and hot_pixel_k <= 0:
+        raise ValueError("k must be positive")
     velocity_domain(tau, params.epsilon)
     start = time.perf_counter()
     ctx, _, n = load_bin_resident(data, ctx)
+    if n and hot_pixel_k is not None:
+        kept, thr = ctypes.c_int64(), ctypes.c_double()
+        rc = ctx.lib.evd_stream_remove_hot_pixels(ctx.h, float(hot_pixel_k), ctypes.byref(kept),
+                                                  ctypes.byref(thr))
+        if rc:
+            _raise(ctx, rc)
+        n = kept.value
+    if rescale_to is not None:
+        rc = ctx.lib.evd_stream_rescale(ctx.h, rescale_to.width, rescale_to.height)
+        if rc:
+            _raise(ctx, rc)
     if n == 0:
         return []
     return _solve_resident(ctx, tau, params, groups, start)

@@ -18,6 +18,9 @@ Fixtures:
                 batches) and grid_search_oracle results
   synth.json    checksums of the reference simulator's windows for the
                 SURVEY §8(d) configurations (pins paper_2209_13168_b200.synth)
+  preproc.npz   pixel_counts / remove_hot_pixels / rescale_events (events.py:273-313)
+                outputs on test-suite streams, landing streams with injected hot
+                pixels, and rescale targets
   evd1.npz      EVD1 files (parse_event_bin, events.py:186-206): valid bodies
                 (sorted, unsorted with equal timestamps, large t_us) with the
                 reference's decoded arrays, and malformed / invalid bodies
@@ -348,6 +351,80 @@ def make_evd1():
     np.savez_compressed(os.path.join(HERE, "evd1.npz"), **out)
 
 
+# ------------------------------------------------------------------ preprocessing
+def make_preproc():
+    from eventdiv import events as ev
+    rng = np.random.default_rng(4242)
+    cases = []
+
+    def stream(x, y, t, w, h, p=None):
+        x = np.asarray(x, np.float64)
+        p = np.ones(len(x), np.int8) if p is None else np.asarray(p, np.int8)
+        return ev.EventStream(x, np.asarray(y, np.float64), np.asarray(t, np.float64), p,
+                              SensorGeometry(w, h))
+
+    xs, ys = np.meshgrid(np.arange(3) + 0.5, np.arange(3) + 0.5)
+    cases.append(("uniform", stream(xs.ravel(), ys.ravel(), np.arange(9) * 0.01, 8, 8), 5.0))
+    hx, hy, ht, t0 = [], [], [], 0.0
+    for i in range(8):
+        hx.append(i + 0.5); hy.append(0.5); ht.append(t0); t0 += 1e-4
+    for i in range(8):
+        for _ in range(2):
+            hx.append(i + 0.5); hy.append(1.5); ht.append(t0); t0 += 1e-4
+    for _ in range(1000):
+        hx.append(7.5); hy.append(7.5); ht.append(t0); t0 += 1e-4
+    cases.append(("hot", stream(hx, hy, ht, 8, 8), 5.0))
+    n = 2000
+    cases.append(("random8", stream(rng.uniform(0, 8, n), rng.uniform(0, 8, n),
+                                    np.sort(rng.uniform(0, 1, n)), 8, 8,
+                                    rng.choice([-1, 1], n)), 10.0))
+    stream_l, _ = generate_landing_events(SimConfig(
+        z0=1.0, nu=-0.3, geometry=SensorGeometry(64, 48), duration=1.5, n_points=400,
+        event_spacing_px=1.0, seed=9))
+    # inject hot pixels: many events on a few pixels, merged in time order
+    inj_t = np.sort(rng.uniform(0, 1.5, 3000))
+    inj_x = rng.choice([3.5, 40.25, 63.75], 3000)
+    inj_y = rng.choice([1.5, 20.5, 47.5], 3000)
+    allx = np.concatenate([stream_l.x, inj_x]); ally = np.concatenate([stream_l.y, inj_y])
+    allt = np.concatenate([stream_l.t, inj_t]); allp = np.concatenate([stream_l.polarity,
+                                                                       np.ones(3000, np.int8)])
+    order = np.argsort(allt, kind="stable")
+    landing = stream(allx[order], ally[order], allt[order], 64, 48, allp[order])
+    cases.append(("landing_hot10", landing, 10.0))
+    cases.append(("landing_hot3", landing, 3.0))
+    cases.append(("landing_clean", stream_l, 10.0))
+    n = 20000  # dense: median and MAD well above 1, an even count of nonzero pixels
+    dx = np.concatenate([rng.uniform(0, 16, n), np.full(900, 2.5), np.full(700, 13.75)])
+    dy = np.concatenate([rng.uniform(0, 12, n), np.full(900, 7.5), np.full(700, 0.25)])
+    dt = np.sort(rng.uniform(0, 2, len(dx)))
+    perm = rng.permutation(len(dx))
+    dense = stream(dx[perm], dy[perm], dt, 16, 12, rng.choice([-1, 1], len(dx)))
+    cases.append(("dense4", dense, 4.0))
+    cases.append(("dense2_5", dense, 2.5))
+    out, meta = {}, {"hot": [], "rescale": []}
+    for name, st, k in cases:
+        kept = ev.remove_hot_pixels(st, k=k)
+        counts = ev.pixel_counts(st)
+        nz = counts[counts > 0].astype(np.float64)
+        med = np.median(nz); mad = np.median(np.abs(nz - med))
+        for key, arr in (("x", st.x), ("y", st.y), ("t", st.t), ("p", st.polarity),
+                         ("kx", kept.x), ("ky", kept.y), ("kt", kept.t), ("kp", kept.polarity),
+                         ("counts", counts)):
+            out[f"{name}_{key}"] = arr
+        meta["hot"].append({"name": name, "w": st.geometry.width, "h": st.geometry.height,
+                            "k": k, "threshold": bits(float(med + k * mad))})
+    for name, st, (w2, h2) in (("land_half", stream_l, (32, 24)), ("land_odd", stream_l, (97, 61)),
+                               ("example", stream([640.0], [380.0], [0.0], 1280, 760), (160, 90))):
+        r = ev.rescale_events(st, SensorGeometry(w2, h2))
+        for key, arr in (("x", st.x), ("y", st.y), ("t", st.t), ("p", st.polarity),
+                         ("rx", r.x), ("ry", r.y)):
+            out[f"{name}_{key}"] = arr
+        meta["rescale"].append({"name": name, "w": st.geometry.width, "h": st.geometry.height,
+                                "w2": w2, "h2": h2})
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(os.path.join(HERE, "preproc.npz"), **out)
+
+
 # ------------------------------------------------------------------ synth
 def make_synth():
     out = {}
@@ -364,7 +441,7 @@ def make_synth():
 
 if __name__ == "__main__":
     big = "--big" in sys.argv
-    what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["segments", "images", "bnb", "synth", "evd1"]
+    what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["segments", "images", "bnb", "synth", "evd1", "preproc"]
     if "segments" in what:
         make_segments()
     if "images" in what:
@@ -373,5 +450,7 @@ if __name__ == "__main__":
         make_synth()
     if "evd1" in what:
         make_evd1()
+    if "preproc" in what:
+        make_preproc()
     if "bnb" in what:
         make_bnb(big)

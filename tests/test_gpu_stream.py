@@ -111,3 +111,55 @@ def test_bin_to_samples_equals_host_pipeline(tmp_path):
                                           params)
     dev = evd.stream_divergence_bin(data, params)
     assert len(dev) > 4 and _key(dev) == _key(host)
+
+
+# ------------------------------------------------------------------ preprocessing
+def _preproc():
+    import json
+    import os
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "preproc.npz"))
+    return z, json.loads(bytes(z["meta"]).decode())
+
+
+def _as_stream(z, n, w, h):
+    from paper_2209_13168_b200.events import SensorGeometry
+    return EventStream(z[f"{n}_x"], z[f"{n}_y"], z[f"{n}_t"], z[f"{n}_p"], SensorGeometry(w, h))
+
+
+def test_preprocessing_matches_reference():
+    from paper_2209_13168_b200.events import SensorGeometry
+    z, meta = _preproc()
+    for c in meta["hot"]:
+        n = c["name"]
+        s = _as_stream(z, n, c["w"], c["h"])
+        assert np.array_equal(evd.pixel_counts(s), z[f"{n}_counts"]), n
+        kept = evd.remove_hot_pixels(s, k=c["k"])
+        for attr, key in (("x", "kx"), ("y", "ky"), ("t", "kt"), ("polarity", "kp")):
+            assert np.array_equal(getattr(kept, attr), z[f"{n}_{key}"]), (n, key)
+    for c in meta["rescale"]:
+        n = c["name"]
+        r = evd.rescale_events(_as_stream(z, n, c["w"], c["h"]), SensorGeometry(c["w2"], c["h2"]))
+        assert np.array_equal(r.x, z[f"{n}_rx"]) and np.array_equal(r.y, z[f"{n}_ry"]), n
+        assert (r.geometry.width, r.geometry.height) == (c["w2"], c["h2"])
+    with pytest.raises(ValueError):
+        evd.remove_hot_pixels(_as_stream(z, "hot", 8, 8), k=0)
+
+
+def test_bin_preprocessed_pipeline_equals_host(tmp_path):
+    """EVD1 bytes -> hot-pixel removal -> rescale -> windows -> solves, all on the
+    device, equals the host composition of the same steps."""
+    from paper_2209_13168_b200.events import SensorGeometry
+    s = _stream()
+    hot = (np.abs(s.x - 10.5) < 0.5) & (np.abs(s.y - 8.5) < 0.5)
+    keep = ~hot | (np.arange(s.n) % 2 == 0)
+    s = EventStream(s.x[keep], s.y[keep], s.t[keep], s.polarity[keep], s.geometry)
+    path = tmp_path / "s.bin"
+    evd.write_event_bin(s, path)
+    data = path.read_bytes()
+    params = evd.SolverParams()
+    target = SensorGeometry(80, 60)
+    host_stream = evd.rescale_events(evd.remove_hot_pixels(evd.parse_event_bin(data), k=8.0), target)
+    host = evd.estimate_stream_divergence(evd.batch_stream(host_stream, 0.5), params)
+    dev = evd.stream_divergence_bin(data, params, hot_pixel_k=8.0, rescale_to=target)
+    assert _key(dev) == _key(host)

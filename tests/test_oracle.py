@@ -113,3 +113,24 @@ def test_evd1_oracle_matches_reference_parser():
         with pytest.raises(cls[kind]) as ei:
             orc.parse_bin(z[f"bad_{name}_data"].tobytes())
         assert str(ei.value) == msg
+
+
+def _preproc_golden():
+    z = np.load(os.path.join(GOLDEN, "preproc.npz"))
+    return z, json.loads(bytes(z["meta"]).decode())
+
+
+def test_preprocessing_oracle_matches_reference():
+    z, meta = _preproc_golden()
+    for c in meta["hot"]:
+        n = c["name"]
+        x, y, t, p = (z[f"{n}_{k}"] for k in ("x", "y", "t", "p"))
+        assert np.array_equal(orc.pixel_counts(x, y, c["w"], c["h"]), z[f"{n}_counts"])
+        kx, ky, kt, kp, thr = orc.remove_hot_pixels(x, y, t, p, c["w"], c["h"], c["k"])
+        for got, key in ((kx, "kx"), (ky, "ky"), (kt, "kt"), (kp, "kp")):
+            assert np.array_equal(got, z[f"{n}_{key}"]), (n, key)
+        assert thr == f64(c["threshold"])
+    for c in meta["rescale"]:
+        n = c["name"]
+        rx, ry = orc.rescale(z[f"{n}_x"], z[f"{n}_y"], c["w"], c["h"], c["w2"], c["h2"])
+        assert np.array_equal(rx, z[f"{n}_rx"]) and np.array_equal(ry, z[f"{n}_ry"])
