@@ -216,7 +216,11 @@ int ensure_tree(evd_ctx *ctx, long long M, int cuts_target)
         pcuts(v, 0, T, cuts);
         long long worst = 0;
         for (int c : cuts) worst = std::max<long long>(worst, 2 * (v[c].n / 64 + 1));
-        if (worst <= kCutSmem && 2 * (long long)cuts.size() <= kCutSmem) break;
+        // at most one cut per CTA: a CTA that owned two would evaluate them
+        // back to back on every node's critical path (measured ~3 us/node)
+        if (worst <= kCutSmem && 2 * (long long)cuts.size() <= kCutSmem &&
+            (long long)cuts.size() <= std::max(cuts_target, 1))
+            break;
         if (worst > kCutSmem) {
             if (2 * (long long)cuts.size() > kCutSmem)
                 return fail(ctx, EVD_ERR_ARG, "image size %lld too large for the reduction plan", M);
