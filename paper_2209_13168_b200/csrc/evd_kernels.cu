@@ -75,7 +75,7 @@ struct WarpQueue {
     long long ev[64];       // uncertain events awaiting the exact path
     SegDesc d[64];
     unsigned int *img[64];  // image each queued segment marks
-    int off[33];  // exclusive prefix of chunk counts per lane
+    int off[65];  // exclusive prefix of chunk counts (per lane, or per slot for warp_drain_list)
     int na[32];   // chunks of the lane's first segment
 };
 
@@ -162,6 +162,52 @@ __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int 
             active = cursor_init(q.d[slot], second ? r - q.na[L] : r, c);
         }
         const SegDesc d = q.d[slot];  // in registers for the walk
+        while (__any_sync(0xffffffffu, active))
+            if (active) active = cursor_step(d, c, W, H, sink, marks);
+    }
+    __syncwarp();
+    return marks;
+}
+
+// Sample the nq (< 64) segments pooled in slots [0, nq), in rounds of 32
+// chunks.  Callers pool segments over several events and drain once 32 are
+// waiting, so rounds run with full lanes.
+__device__ __noinline__ int warp_drain_list(WarpQueue &q, int nq, int W, int H)
+{
+    const int lane = threadIdx.x & 31;
+    const int c0 = lane < nq ? q.d[lane].chunks : 0;
+    const int c1 = lane + 32 < nq ? q.d[lane + 32].chunks : 0;
+    int i0 = c0, i1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v0 = __shfl_up_sync(0xffffffffu, i0, o);
+        const int v1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) { i0 += v0; i1 += v1; }
+    }
+    const int t0 = __shfl_sync(0xffffffffu, i0, 31);
+    i1 += t0;
+    q.off[lane] = i0 - c0;
+    q.off[lane + 32] = i1 - c1;
+    const int total = __shfl_sync(0xffffffffu, i1, 31);
+    if (lane == 0) q.off[64] = total;
+    __syncwarp();
+    int marks = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int t = base + lane;
+        bool active = false;
+        int slot = 0;
+        Cursor c;
+        AtomicSink sink{nullptr};
+        if (t < total) {
+            int L = 0;  // largest slot with off[L] <= t (empty slots share offsets)
+#pragma unroll
+            for (int s = 32; s > 0; s >>= 1)
+                if (L + s < 64 && q.off[L + s] <= t) L += s;
+            slot = L;
+            sink.img = q.img[slot];
+            active = cursor_init(q.d[slot], t - q.off[L], c);
+        }
+        const SegDesc d = q.d[slot];
         while (__any_sync(0xffffffffu, active))
             if (active) active = cursor_step(d, c, W, H, sink, marks);
     }
@@ -285,6 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
     if (threadIdx.x < kFrontGroup) s_fi[threadIdx.x] = 0;
     __syncthreads();
     unsigned long long fi = 0;
+    int nq = 0;  // segments pooled in wq (warp-uniform)
     const long long gw = (long long)tb * wpb + warp, nw = (long long)bpg * wpb;
     for (long long e = gw; e < n; e += nw) {
         const double x = __ldg(xc + e), y = __ldg(yc + e), tt = __ldg(t + e);
@@ -293,12 +340,29 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
         a.x = __shfl_up_sync(0xffffffffu, b.x, 1);
         a.y = __shfl_up_sync(0xffffffffu, b.y, 1);
         if (!shared_lo) a = warp_event(x, y, tt, my_lo, my_dlo, cx, cy);
+        // pool multi-pixel segments over events; drain 32+ at a time
+        SegDesc d;
         int c = 0, m = 0;
         if (valid) {
             fi += fully_inside(a.x, a.y, b.x, b.y, W, H);
-            c = segment_or_queue_inl<EVD_FRONT_INLINE>(a.x, a.y, b.x, b.y, W, H, wq, 2 * lane, sink, m);
+            c = build_segment(a.x, a.y, b.x, b.y, W, H, kChunk, d, sink, m);
         }
-        if (__any_sync(0xffffffffu, c != 0)) warp_drain(wq, c, 0, W, H);
+        const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
+        if (c > 0) {
+            const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+            wq.d[slot] = d;
+            wq.img[slot] = img;
+        }
+        nq += __popc(bal);
+        if (nq >= 32) {
+            __syncwarp();
+            warp_drain_list(wq, nq, W, H);
+            nq = 0;
+        }
+    }
+    if (nq > 0) {
+        __syncwarp();
+        warp_drain_list(wq, nq, W, H);
     }
     if (valid && fi) atomicAdd(s_fi + lane, fi);
     __syncthreads();
