@@ -4,6 +4,7 @@
 // image size, the libm pow table for the bound assembly, and the launch of the
 // device-resident branch and bound.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -789,9 +790,11 @@ namespace {
 
 // Run the device-resident BnB over n_windows windows of the resident events
 // (window w = events [off[w], off[w+1])) with `groups` independent CTA groups.
-// windows at least this large use the filtered event path (measured: a win at
-// ~1M events, a loss at ~200k where register pressure dominates)
-constexpr long long kFilterMinEvents = 500000;
+// The filtered event path (approximate warps certified by error margins,
+// exact fallback) was a win at ~1M events before the sampler's position-based
+// chunks; it now measures 1-3% slower at every size (cfg 1, 2, 3, 5), so it is
+// off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
+constexpr long long kFilterMinEvents = LLONG_MAX;
 
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
