@@ -162,6 +162,27 @@ __device__ __forceinline__ int mark_point(double px, double py, int W, int H, Pr
     return marks;
 }
 
+// mark_point for a point that is usually inside one pixel (a midpoint
+// between consecutive crossings): the single-cell case tests one pixel;
+// points on a grid line take the general path.
+template <class Sink>
+__device__ __forceinline__ int mark_interior(double px, double py, int W, int H, Prev &prev,
+                                             Sink &sink)
+{
+    const double fx = floor(px), fy = floor(py);
+    if (px != fx && py != fy) {
+        const int ix = (int)fx, iy = (int)fy;
+        const bool seen = ix >= prev.x0 && ix <= prev.x1 && iy >= prev.y0 && iy <= prev.y1;
+        prev = Prev{ix, ix, iy, iy};
+        if (!seen && (unsigned)ix < (unsigned)W && (unsigned)iy < (unsigned)H) {
+            sink(iy * W + ix);
+            return 1;
+        }
+        return 0;
+    }
+    return mark_point(px, py, W, H, prev, sink);
+}
+
 // One monotone list of grid-line crossing parameters along the clipped segment
 // (contrast.py:150-175): item i is s = clamp01((k_i - c0) / dd) for the
 // integers k in [ceil(min), floor(max)], enumerated in increasing-s order
@@ -424,7 +445,7 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
         c.fin = 1;
     }
     const double sm = dmul(0.5, dadd(c.cur, nxt));
-    marks += mark_point(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
+    marks += mark_interior(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
     c.cur = nxt;
     return --c.left > 0;
 }
