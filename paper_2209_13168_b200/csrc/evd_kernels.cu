@@ -32,6 +32,9 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #define EVD_FRONT_INLINE 6
 #endif
 constexpr int kChunk = EVD_CHUNK;
+#ifndef EVD_BATCH_DIV
+#define EVD_BATCH_DIV 1
+#endif
 #ifndef EVD_GUIDED_WIDTH
 #define EVD_GUIDED_WIDTH (1.0 / 16)
 #endif
@@ -706,8 +709,13 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
     // together; the sampler still spreads a small batch's chunks over all
     // 32 lanes.
     const long long warps = gsz >> 5;
-    long long base = j.gb * (long long)blockDim.x + (threadIdx.x & ~31);
-    int size = 32;
+    // batches of up to 32 events, fewer when the window cannot give every warp
+    // one full batch: a small window is latency-bound, and more, shorter
+    // batches keep all warps busy (cfg 1: 20k events on 2368 warps)
+    long long fb = n / (EVD_BATCH_DIV * warps);
+    const int first = (int)(fb < 4 ? 4 : (fb > 32 ? 32 : fb));
+    long long base = (j.gb * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * first;
+    int size = first;
     while (base < n) {
         const long long i = base + lane;
         int cA = 0, cB = 0, dummy = 0;
@@ -738,10 +746,10 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
             // claim size from the remaining events as last seen by this warp
             const long long rem = n - base;
             long long s = rem / (2 * warps);
-            size = (int)(s < 4 ? 4 : (s > 32 ? 32 : s));
+            size = (int)(s < 4 ? 4 : (s > first ? first : s));
         }
         long long nb = 0;
-        if (lane == 0) nb = gsz + (long long)atomicAdd(acc + 7, (unsigned long long)size);
+        if (lane == 0) nb = warps * first + (long long)atomicAdd(acc + 7, (unsigned long long)size);
         base = __shfl_sync(0xffffffffu, nb, 0);
     }
 }
