@@ -28,9 +28,6 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #ifndef EVD_CHUNK
 #define EVD_CHUNK 16
 #endif
-#ifndef EVD_FRONT_INLINE
-#define EVD_FRONT_INLINE 6
-#endif
 constexpr int kChunk = EVD_CHUNK;
 #ifndef EVD_BATCH_DIV
 #define EVD_BATCH_DIV 1
@@ -83,14 +80,10 @@ struct WarpQueue {
 };
 
 // Build one segment and queue it in the lane's shared-memory slot for
-// warp_drain (single-pixel and off-frame segments finish in build_segment);
-// segments with at most INLINE crossings are sampled by their own lane.
-// Returns the number of queued chunks.  The solve kernel queues everything
-// (INLINE = -1): its lanes hold unrelated events, so in-lane sampling diverges,
-// and the extra sampler copy costs registers and I-cache (measured slower).
-// The frontier kernel's lanes hold one event at neighbouring intervals --
-// segments of nearly equal length -- and keeps short ones in the lane.
-template <int INLINE>
+// warp_drain (single-pixel and off-frame segments finish in build_segment).
+// Returns the number of queued chunks.  Every multi-pixel segment is queued:
+// a lane sampling its own short segment diverges from the others, and the
+// extra sampler copy costs registers and I-cache (measured slower).
 __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double bx, double by,
                                                     int W, int H, WarpQueue &q, int slot,
                                                     AtomicSink &sink, int &marks)
@@ -98,10 +91,6 @@ __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double
     SegDesc d;
     const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
     if (c == 0) return 0;
-    if (INLINE >= 0 && d.X.n + d.Y.n <= INLINE) {
-        marks += sample_chunk(d, 0, W, H, sink);
-        return 0;
-    }
     q.d[slot] = d;
     q.img[slot] = sink.img;
     return c;
@@ -117,7 +106,7 @@ __device__ __noinline__ int segment_or_queue_ool(double ax, double ay, double bx
 {
     AtomicSink sink{img};
     int marks = 0;
-    const int c = segment_or_queue_inl<-1>(ax, ay, bx, by, W, H, q, slot, sink, marks);
+    const int c = segment_or_queue_inl(ax, ay, bx, by, W, H, q, slot, sink, marks);
     return c | (marks << 16);  // chunks < 2^16 (W + H + 4 items / kChunk)
 }
 __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
