@@ -836,6 +836,7 @@ __device__ __forceinline__ void replica_push(const SolveArgs &a, Replica &R, lon
 // with >=, the iteration cap, then the best-first pop and stop test of the
 // next iteration.  Whole block; identical in every block.  Frontier entries
 // [0, fr_n) are in `view` when fr_n <= kFrView (else read from global).
+template <bool FILTER>
 __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const FrontierEntry *view,
                          FrontierEntry *fr)
 {
@@ -883,11 +884,19 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
         return staged ? view[i] : entry_load(fr + i);
     };
     // best-first pop: argmax over the committed entries and this step's pushes
+    // (by warp 0 alone for a frontier of up to 256 entries: no cross-warp pass)
+    const bool small = n1 <= 256;
+    if (small && threadIdx.x >= 32) {
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
     __shared__ double r_b[32];
     __shared__ long long r_c[32], r_i[32];
     double bb = -DBL_MAX;
     long long bc = LLONG_MAX, bi = -1;
-    for (long long i = threadIdx.x; i < n1; i += blockDim.x) {
+    const int stride = small ? 32 : (int)blockDim.x;
+    for (long long i = threadIdx.x; i < n1; i += stride) {
         double b;
         long long c;
         if (i >= n0) { b = R.pushed[i - n0].bound; c = R.pushed[i - n0].counter; }
@@ -903,10 +912,10 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
         if (oi >= 0 && (bi < 0 || better(ob, oc, bb, bc))) { bb = ob; bc = oc; bi = oi; }
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) { r_b[wid] = bb; r_c[wid] = bc; r_i[wid] = bi; }
+    if (!small && lane == 0) { r_b[wid] = bb; r_c[wid] = bc; r_i[wid] = bi; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+        for (int w = 1; !small && w < (int)(blockDim.x >> 5); w++)
             if (r_i[w] >= 0 && (bi < 0 || better(r_b[w], r_c[w], bb, bc))) {
                 bb = r_b[w]; bc = r_c[w]; bi = r_i[w];
             }
@@ -932,9 +941,11 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
             R.den_lo = dadd(1.0, dmul(top.lo, a.tau));
             R.den_c = dadd(1.0, dmul(c, a.tau));
             R.den_hi = dadd(1.0, dmul(top.hi, a.tau));
-            R.r_lo = ddiv(1.0, R.den_lo);
-            R.r_c = ddiv(1.0, R.den_c);
-            R.r_hi = ddiv(1.0, R.den_hi);
+            if (FILTER) {  // the filtered path's approximate warps
+                R.r_lo = ddiv(1.0, R.den_lo);
+                R.r_c = ddiv(1.0, R.den_c);
+                R.r_hi = ddiv(1.0, R.den_hi);
+            }
             R.mode = kModeNode;
         }
     }
@@ -1304,7 +1315,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             if (tr) bclock(a, it, 10);
             const double S = top_combine(tree, scratch);
             if (tr) bclock(a, it, 11);
-            bnb_step(a, R, S, view, fr);
+            bnb_step<FILTER>(a, R, S, view, fr);
             if (tr) bclock(a, it, 12);
             if (threadIdx.x == 0) R.parity = par ^ 1;
             if (tr && gb == 0) trace_point(a, it, kTrB0Step1);
