@@ -264,7 +264,7 @@ int ensure_tree(evd_ctx *ctx, long long M, int cuts_target)
                 level_h = rel;
             }
             trip.push_back(make_int4((int)(lv.size() + i), find_local(v[id].l),
-                                     find_local(v[id].r), 0));
+                                     find_local(v[id].r), lvl));  // .w: level
         }
         const int nlev = in.empty() ? 0 : lvl + 1;
         L[nlev] = (int)in.size();
@@ -293,7 +293,8 @@ int ensure_tree(evd_ctx *ctx, long long M, int cuts_target)
                 top_lvl.push_back((int)i);
                 cur_h = top_h[order[i]];
             }
-            top.push_back(make_int4(top_index[id], top_index[v[id].l], top_index[v[id].r], 0));
+            top.push_back(make_int4(top_index[id], top_index[v[id].l], top_index[v[id].r],
+                                    (int)top_lvl.size() - 1));  // .w: level
         }
         top_levels = (int)top_lvl.size();
         top_lvl.push_back((int)order.size());

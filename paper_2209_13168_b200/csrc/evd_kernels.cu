@@ -476,12 +476,21 @@ __device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc,
     const int t0 = T.cut_trip0[c], ni = T.cut_trip0[c + 1] - t0;
     const int *lvl = T.cut_lvl + (long long)c * (kMaxLevels + 1);
     const int nlev = T.cut_nlev[c];
-    for (int h = 0; h < nlev; h++) {
-        for (int k = lvl[h] + threadIdx.x; k < lvl[h + 1]; k += blockDim.x) {
-            const int4 tr = T.trip[t0 + k];
-            loc[tr.x] = dadd(loc[tr.y], loc[tr.z]);
+    if (ni <= (int)blockDim.x) {
+        // one internal node per thread, loaded once; its level is in .w
+        const int4 tr = threadIdx.x < ni ? T.trip[t0 + threadIdx.x] : make_int4(0, 0, 0, -1);
+        for (int h = 0; h < nlev; h++) {
+            if (tr.w == h) loc[tr.x] = dadd(loc[tr.y], loc[tr.z]);
+            __syncthreads();
         }
-        __syncthreads();
+    } else {
+        for (int h = 0; h < nlev; h++) {
+            for (int k = lvl[h] + threadIdx.x; k < lvl[h + 1]; k += blockDim.x) {
+                const int4 tr = T.trip[t0 + k];
+                loc[tr.x] = dadd(loc[tr.y], loc[tr.z]);
+            }
+            __syncthreads();
+        }
     }
     const double r = loc[ni > 0 ? nl + ni - 1 : 0];
     __syncthreads();
@@ -1022,12 +1031,22 @@ __device__ TreeDev cache_tree(const TreeDev &g, TreeCache &tc, bool &local, int 
 // Combine the C cut sums (already staged in v) through the top of the tree.
 __device__ double top_combine(const TreeDev &T, double *v)
 {
-    for (int h = 0; h < T.top_levels; h++) {
-        for (int k = T.top_lvl[h] + threadIdx.x; k < T.top_lvl[h + 1]; k += blockDim.x) {
-            const int4 tr = T.top[k];
-            v[tr.x] = dadd(v[tr.y], v[tr.z]);
+    const int levels = T.top_levels, ntop = T.top_lvl[levels];
+    if (ntop <= (int)blockDim.x) {
+        // one internal node per thread, loaded once; its level is in .w
+        const int4 tr = threadIdx.x < ntop ? T.top[threadIdx.x] : make_int4(0, 0, 0, -1);
+        for (int h = 0; h < levels; h++) {
+            if (tr.w == h) v[tr.x] = dadd(v[tr.y], v[tr.z]);
+            __syncthreads();
         }
-        __syncthreads();
+    } else {
+        for (int h = 0; h < levels; h++) {
+            for (int k = T.top_lvl[h] + threadIdx.x; k < T.top_lvl[h + 1]; k += blockDim.x) {
+                const int4 tr = T.top[k];
+                v[tr.x] = dadd(v[tr.y], v[tr.z]);
+            }
+            __syncthreads();
+        }
     }
     const double r = v[T.top_root];
     __syncthreads();
