@@ -29,6 +29,7 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #define EVD_CHUNK 16
 #endif
 constexpr int kChunk = EVD_CHUNK;
+constexpr int kPixCutThreads = 128;  // pixel phase: threads walking the point image's cut
 #ifndef EVD_BATCH_DIV
 #define EVD_BATCH_DIV 1
 #endif
@@ -443,16 +444,29 @@ struct SqF64 {
     }
 };
 
-// Evaluate cut subtree c of the pairwise tree with the whole block; returns
-// the subtree sum to every thread.
+// Evaluate cut subtree c of the pairwise tree with threads [0, nt) of the
+// block (a warp multiple) synchronised by `bar`; returns the subtree sum to
+// every participating thread.
+struct BlockBar {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct NamedBar {  // hardware barrier `id` over the first `nt` threads
+    int id, nt;
+    __device__ __forceinline__ void operator()() const
+    {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+    }
+};
 __device__ __forceinline__ void bclock(const SolveArgs &a, long long it, int k);
-template <class Q>
+template <class Q, class Bar = BlockBar>
 __device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc,
-                           const SolveArgs &dbg_a, long long dbg_it)
+                           const SolveArgs &dbg_a, long long dbg_it, int nt = -1,
+                           const Bar &bar = Bar{})
 {
     if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 19);
+    if (nt < 0) nt = blockDim.x;
     const int l0 = T.cut_leaf0[c], nl = T.cut_leaf0[c + 1] - l0;
-    const int j = threadIdx.x & 7, ngroups = blockDim.x >> 3;
+    const int j = threadIdx.x & 7, ngroups = nt >> 3;
     if (kTraceBuild && dbg_a.btrace) {
         asm volatile("" ::"r"(nl));
         bclock(dbg_a, dbg_it, 16);
@@ -471,29 +485,29 @@ __device__ double eval_cut(const TreeDev &T, int c, const Q &q, double *loc,
         if (j == 0) loc[i] = v;
     }
     if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 14);
-    __syncthreads();
+    bar();
     if (kTraceBuild && dbg_a.btrace) bclock(dbg_a, dbg_it, 15);
     const int t0 = T.cut_trip0[c], ni = T.cut_trip0[c + 1] - t0;
     const int *lvl = T.cut_lvl + (long long)c * (kMaxLevels + 1);
     const int nlev = T.cut_nlev[c];
-    if (ni <= (int)blockDim.x) {
+    if (ni <= nt) {
         // one internal node per thread, loaded once; its level is in .w
         const int4 tr = threadIdx.x < ni ? T.trip[t0 + threadIdx.x] : make_int4(0, 0, 0, -1);
         for (int h = 0; h < nlev; h++) {
             if (tr.w == h) loc[tr.x] = dadd(loc[tr.y], loc[tr.z]);
-            __syncthreads();
+            bar();
         }
     } else {
         for (int h = 0; h < nlev; h++) {
-            for (int k = lvl[h] + threadIdx.x; k < lvl[h + 1]; k += blockDim.x) {
+            for (int k = lvl[h] + threadIdx.x; k < lvl[h + 1]; k += nt) {
                 const int4 tr = T.trip[t0 + k];
                 loc[tr.x] = dadd(loc[tr.y], loc[tr.z]);
             }
-            __syncthreads();
+            bar();
         }
     }
     const double r = loc[ni > 0 ? nl + ni - 1 : 0];
-    __syncthreads();
+    bar();
     return r;
 }
 
@@ -1284,24 +1298,48 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             __syncthreads();
             const double mu = R.mu;
             if (tr) bclock(a, it, 13);
-            for (int cut = gb, q = 0; cut < tree.C; cut += GB, q++) {
-                const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{P, mu}}, scratch,
-                                          a, tr ? it : kBTraceIters);
-                if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
+            // the point image's cut walk (first kPixCutThreads threads, named
+            // barrier 1) runs beside the segment images' sums of squares (the
+            // other warps, named barrier 2): independent latency chains
+            if (threadIdx.x < kPixCutThreads) {
+                for (int cut = gb, q = 0; cut < tree.C; cut += GB, q++) {
+                    const double r = eval_cut(tree, local_cuts ? q : cut, SqU32Clear{{P, mu}}, scratch,
+                                              a, tr ? it : kBTraceIters, kPixCutThreads,
+                                              NamedBar{1, kPixCutThreads});
+                    if (threadIdx.x == 0) __stcg(tree.cutval + cut, r);
+                }
+                if (threadIdx.x == 0) {  // pow(fi/M, 2) table values, needed by the step
+                    R.p2A = __ldg(a.pow2 + R.fiA);
+                    R.p2B = __ldg(a.pow2 + R.fiB);
+                }
+            } else {
+                const int nt2 = blockDim.x - kPixCutThreads;
+                const long long t2 = gb * (long long)nt2 + (threadIdx.x - kPixCutThreads);
+                const long long s2 = (long long)GB * nt2;
+                unsigned long long ws[2] = {0, 0};
+                for (long long p = t2; p < tree.M; p += s2) {
+                    const unsigned long long ha = __ldcg(A + p), hb = __ldcg(B + p);
+                    if (ha) { ws[0] += ha * ha; A[p] = 0u; }
+                    if (hb) { ws[1] += hb * hb; B[p] = 0u; }
+                }
+                __shared__ unsigned long long s_ws[32][2];
+                const int wid = threadIdx.x >> 5;
+                ws[0] = warp_sum(ws[0]);
+                ws[1] = warp_sum(ws[1]);
+                if (lane == 0) { s_ws[wid][0] = ws[0]; s_ws[wid][1] = ws[1]; }
+                asm volatile("bar.sync 2, %0;" ::"r"(nt2) : "memory");
+                if (threadIdx.x == kPixCutThreads) {
+                    unsigned long long x0 = 0, x1 = 0;
+                    for (int w2 = kPixCutThreads >> 5; w2 < (int)(blockDim.x >> 5); w2++) {
+                        x0 += s_ws[w2][0];
+                        x1 += s_ws[w2][1];
+                    }
+                    if (x0) atomicAdd(acc + 4, x0);
+                    if (x1) atomicAdd(acc + 5, x1);
+                }
             }
             if (tr) bclock(a, it, 6);
-            unsigned long long ws[2] = {0, 0};
-            for (long long p = gtid; p < tree.M; p += gsz) {
-                const unsigned long long ha = __ldcg(A + p), hb = __ldcg(B + p);
-                if (ha) { ws[0] += ha * ha; A[p] = 0u; }
-                if (hb) { ws[1] += hb * hb; B[p] = 0u; }
-            }
-            if (threadIdx.x == 0) {  // pow(fi/M, 2) table values, needed by the step
-                R.p2A = __ldg(a.pow2 + R.fiA);
-                R.p2B = __ldg(a.pow2 + R.fiB);
-            }
             if (tr) bclock(a, it, 7);
-            block_add_u64<2>(ws, acc + 4);
             if (tr) bclock(a, it, 8);
             if (tr && gb == 0) trace_point(a, it, kTrB0Pixels1);
             if (tr) trace_max(a, it, kTrPixelsMax);
