@@ -29,7 +29,10 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #define EVD_CHUNK 16
 #endif
 constexpr int kChunk = EVD_CHUNK;
-constexpr int kPixCutThreads = 128;  // pixel phase: threads walking the point image's cut
+#ifndef EVD_PIX_CUT_THREADS
+#define EVD_PIX_CUT_THREADS 128
+#endif
+constexpr int kPixCutThreads = EVD_PIX_CUT_THREADS;  // pixel phase: threads walking the point image's cut
 #ifndef EVD_BATCH_DIV
 #define EVD_BATCH_DIV 1
 #endif
