@@ -796,6 +796,7 @@ namespace {
 // chunks; it now measures 1-3% slower at every size (cfg 1, 2, 3, 5), so it is
 // off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
 constexpr long long kFilterMinEvents = LLONG_MAX;
+constexpr long long kSpecMaxEvents = 500000;  // speculative rounds for windows below this
 
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
@@ -818,12 +819,17 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     const int GB = ctx->solve_blocks / groups;
     long long max_n = 0;
     for (int w = 0; w < n_windows; w++) max_n = std::max(max_n, off[w + 1] - off[w]);
-    if ((rc = ensure_tree(ctx, M, GB))) return rc;
+    // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
+    // trace is on (k_solve has the probes)
+    // (2 slots measured best below ~0.5M events per window on the whole grid;
+    // the wide nodes of larger windows make speculation cost more than the
+    // rounds it saves, and small CTA groups have little fixed cost to save)
+    int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? 2 : 1;
+    if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
+    if (ctx->trace_on) spec_k = 1;
     if ((rc = ensure_pow2(ctx, M, max_n))) return rc;
-    CU(ctx->tree.cutval.ensure((size_t)ctx->tree.dev.C * groups));
-    ctx->tree.dev.cutval = ctx->tree.cutval.p;
-    if (ctx->simg.cap < (size_t)(3 * M * groups)) {  // the kernel leaves them zeroed
-        CU(ctx->simg.ensure((size_t)(3 * M * groups)));
+    if (ctx->simg.cap < (size_t)(3 * kSpecK * M * groups)) {  // the kernels leave them zeroed
+        CU(ctx->simg.ensure((size_t)(3 * kSpecK * M * groups)));
         CU(cudaMemsetAsync(ctx->simg.p, 0, ctx->simg.cap * sizeof(unsigned int), ctx->stream));
     }
     CU(ctx->state.ensure(groups));
@@ -846,6 +852,10 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     for (int w = 0; w < n_windows; w++) todo[w] = w;
     float total_ms = 0.f;
     while (true) {
+        // cut plan: one cut per CTA, or per (slot, CTA) pair for speculative rounds
+        if ((rc = ensure_tree(ctx, M, spec_k > 1 ? std::max(1, GB / spec_k) : GB))) return rc;
+        CU(ctx->tree.cutval.ensure((size_t)ctx->tree.dev.C * kSpecK * groups));
+        ctx->tree.dev.cutval = ctx->tree.cutval.p;
         CU(ctx->frontier.ensure((size_t)(cap * groups)));
         CU(cudaMemsetAsync(ctx->bar2.p, 0, 2 * groups * sizeof(unsigned long long), ctx->stream));
         CU(cudaMemsetAsync(ctx->wres.p, 0, n_windows * sizeof(WindowResult), ctx->stream));
@@ -884,8 +894,10 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         a.btrace = ctx->trace_on ? ctx->btrace.p : nullptr;
         a.filter = (max_n >= kFilterMinEvents) ? 1 : 0;
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
+        a.spec_k = spec_k;
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU(launch_solve(a, groups * GB, ctx->stream));
+        CU((spec_k > 1 || getenv("EVD_SPEC_FORCE")) ? launch_solve_spec(a, groups * GB, ctx->stream)
+                      : launch_solve(a, groups * GB, ctx->stream));
         LAUNCHED(1);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
         std::vector<WindowResult> got(n_windows);
@@ -895,10 +907,15 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         total_ms += ms;
-        bool again = false;
+        bool again = false, overflow = false;
         for (int w : todo) {
             out[w] = got[w];
             if (got[w].status == kStatusCapacity) again = true;
+            if (got[w].status == kStatusSpecOverflow) overflow = true;
+        }
+        if (overflow) {  // the shared-memory frontier filled up: rerun without speculation
+            spec_k = 1;
+            continue;
         }
         if (!again) break;
         cap *= 8;  // frontier outgrew its buffer: rerun (the solve is deterministic)

@@ -49,10 +49,13 @@ struct SolveState {
     long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
     int status, pad;
     unsigned long long marks;  // pixel increments of all images over the solve
+    // speculative rounds (k_solve_spec): per-slot accumulators by round parity
+    alignas(16) unsigned long long sacc[2][4][8];
 };
 
 // Result of one window of evd_solve_windows / evd_solve.
-enum WindowStatus : int { kStatusEmpty = 3 };
+enum WindowStatus : int { kStatusEmpty = 3, kStatusSpecOverflow = 4 };
+constexpr int kSpecK = 4;  // node evaluations per speculative round (k_solve_spec)
 struct WindowResult {
     double nu, contrast, bound_gap;
     long long iterations, bound_evals, point_evals, max_fr;
@@ -82,6 +85,7 @@ struct SolveArgs {
     long long trace_iters;
     long long *btrace;            // [kBTraceIters][group_blocks][kBTraceSlots] (or null)
     int filter;                   // use the filtered (approximate-then-exact) event path
+    int spec_k;                   // k_solve_spec: evaluations per round (1..kSpecK)
 };
 
 constexpr int kBTraceIters = 128;
@@ -139,6 +143,7 @@ void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, 
 int solve_grid_blocks(int device);
 int solve_block_threads();
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
+cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, cudaStream_t s);
 cudaError_t decode_bin(const unsigned char *body_dev, long long n, int W, int H, double *x,
                        double *y, double *t, signed char *p, void *scratch, size_t scratch_bytes,
                        unsigned int *flags_dev, unsigned int *flags_host, int *launches,

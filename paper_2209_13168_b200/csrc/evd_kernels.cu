@@ -1398,9 +1398,425 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
     }
 }
 
+// ---------------------------------------------------------------- speculative rounds
+// k_solve_spec: the same best-first BnB, bit for bit, with up to kSpecK node
+// evaluations per round.  Slot 0 is the node the reference pops next; slots
+// 1.. are the best narrow frontier entries, evaluated speculatively (a node's
+// results are a pure function of its interval).  The step then replays the
+// reference's pops in order and consumes cached results until a pop finds
+// none.  At cfg 1/2 a 4-slot round covers ~3.5 pops (the next pops are mostly
+// the frontier's current best, rarely the newest children), so the per-round
+// fixed costs (two grid barriers, the contrast reduction, the step) are paid
+// ~3.5x less often.  The frontier is replicated in every CTA's shared memory.
+constexpr int kSpecFr = 1024;     // frontier entries per CTA (shared memory)
+constexpr int kSpecCache = 64;    // results of evaluated, not yet popped nodes
+constexpr double kSpecWidth = 1.0 / 16;  // only intervals this narrow are speculated
+
+struct SpecSlot {
+    double lo, hi, c, den_lo, den_c, den_hi;
+    long long counter;
+};
+struct SpecRes {
+    long long counter;
+    double C, cbA, cbB;
+};
+struct SpecState {
+    SpecSlot slot[kSpecK];
+    int nslot, mode, done, status, parity;
+    double nu_hat, c_hat, bound_gap;
+    long long iterations, bound_evals, point_evals, next_counter, fr_n, max_fr;
+    unsigned long long marks, exact;
+    double mu[kSpecK];
+    unsigned long long fiA[kSpecK], fiB[kSpecK];
+    double S[kSpecK];
+    SpecRes cache[kSpecCache];
+    int ncache, cache_head;
+    int cur;  // cache index of the node being processed (-1: slot results below)
+};
+
+__device__ __forceinline__ int spec_find(const SpecState &Z, long long counter)
+{
+    for (int k = 0; k < Z.ncache; k++)
+        if (Z.cache[k].counter == counter) return k;
+    return -1;
+}
+
+// warp-0 argmax over the shared frontier, skipping entries flagged by `skip`
+template <class Skip>
+__device__ __forceinline__ long long spec_argmax(const FrontierEntry *fr, long long n, Skip skip)
+{
+    double bb = -DBL_MAX;
+    long long bc = LLONG_MAX, bi = -1;
+    for (long long i = threadIdx.x & 31; i < n; i += 32) {
+        const FrontierEntry &e = fr[i];
+        if (skip(e)) continue;
+        if (bi < 0 || better(e.bound, e.counter, bb, bc)) { bb = e.bound; bc = e.counter; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, bb, o);
+        const long long oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || better(ob, oc, bb, bc))) { bb = ob; bc = oc; bi = oi; }
+    }
+    return bi;
+}
+
+__device__ __forceinline__ void spec_set_slot(const SolveArgs &a, SpecSlot &s,
+                                              const FrontierEntry &e)
+{
+    const double c = dmul(0.5, dadd(e.lo, e.hi));  // VelocityInterval.center
+    s.lo = e.lo;
+    s.hi = e.hi;
+    s.c = c;
+    s.den_lo = dadd(1.0, dmul(e.lo, a.tau));
+    s.den_c = dadd(1.0, dmul(c, a.tau));
+    s.den_hi = dadd(1.0, dmul(e.hi, a.tau));
+    s.counter = e.counter;
+}
+
+__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(SolveArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    double *scratch = reinterpret_cast<double *>(smem);
+    TreeCache &tc = *reinterpret_cast<TreeCache *>(smem + kRegionA);
+    FrontierEntry *frs = reinterpret_cast<FrontierEntry *>(smem + kRegionA + sizeof(TreeCache));
+    __shared__ SpecState Z;
+    __shared__ unsigned long long s_acc[kSpecK][5];
+    __shared__ int s_flag;
+    const int GB = a.group_blocks;
+    const int grp = blockIdx.x / GB, gb = blockIdx.x % GB;
+    if (grp >= a.groups) return;
+    unsigned long long *ctr = a.bar + 2 * grp;
+    unsigned long long target = 0;
+    SolveState *st = a.st + grp;
+    const long long M = a.tree.M;
+    const int K = a.spec_k;
+    unsigned int *img0 = a.img + (long long)grp * 3 * kSpecK * M;  // slot s: P, A, B
+    const int lane = threadIdx.x & 31;
+    const long long gsz = (long long)GB * blockDim.x;
+    const int W = a.W, H = a.H;
+    bool local_cuts;
+    TreeDev gtree = a.tree;
+    gtree.cutval = a.tree.cutval + (long long)grp * kSpecK * a.tree.C;  // [slot][C]
+    // this CTA walks cut (gb mod C) of slot (gb div C) whenever slots x cuts
+    // fit the group (the plan aims at C <= GB / kSpecK): cache that cut
+    __shared__ TreeDev tree_s;
+    {
+        const TreeDev t = cache_tree(gtree, tc, local_cuts, gb % gtree.C, GB);
+        if (threadIdx.x == 0) tree_s = t;
+        __syncthreads();
+    }
+    const TreeDev &tree = tree_s;
+    const int C = tree.C;
+    const int ntop = tree.top_lvl[tree.top_levels];
+
+    for (int w = grp; w < a.n_windows; w += a.groups) {
+        const long long off = a.offsets[w], n = a.offsets[w + 1] - off;
+        if (n == 0) {
+            if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
+            continue;
+        }
+        const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
+        grid_sync(ctr, target, GB);
+        if (gb == 0 && threadIdx.x == 0) {
+            unsigned long long *z = &st->sacc[0][0][0];
+            for (int k = 0; k < 2 * kSpecK * 8; k++) __stcg(z + k, 0ull);
+        }
+        grid_sync(ctr, target, GB);
+        if (threadIdx.x == 0) {
+            Z.slot[0] = SpecSlot{a.lo0, a.hi0, a.c0, a.den_lo0, a.den_c0, a.den_hi0, -1};
+            Z.nslot = 1;
+            Z.mode = kModeRoot;
+            Z.done = 0;
+            Z.status = kStatusOk;
+            Z.parity = 0;
+            Z.nu_hat = Z.c_hat = Z.bound_gap = 0.0;
+            Z.iterations = Z.bound_evals = Z.point_evals = Z.next_counter = Z.fr_n = Z.max_fr = 0;
+            Z.marks = Z.exact = 0;
+            Z.ncache = Z.cache_head = 0;
+        }
+        __syncthreads();
+        while (!Z.done) {
+            const int ns = Z.nslot, mode = Z.mode, par = Z.parity;
+            unsigned long long (*sacc)[8] = st->sacc[par];
+            if (threadIdx.x < kSpecK * 5) (&s_acc[0][0])[threadIdx.x] = 0;
+            __syncthreads();
+            // events: one pass per slot (each with its own work counter)
+            for (int s = 0; s < ns; s++) {
+                const SpecSlot sl = Z.slot[s];
+                unsigned int *P = img0 + (long long)(3 * s) * M, *A = P + M, *B = A + M;
+                unsigned long long v[4] = {0, 0, 0, 0}, vex[1] = {0};
+                EventJob J{xc, yc, tw, n, sl.lo, sl.c, sl.hi, sl.den_lo, sl.den_c, sl.den_hi,
+                           a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
+                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth};
+                event_pass_exact(J, wq, v, vex);
+#pragma unroll
+                for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);
+                vex[0] = warp_sum(vex[0]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        if (v[k]) atomicAdd(&s_acc[s][k], v[k]);
+                    if (vex[0]) atomicAdd(&s_acc[s][4], vex[0]);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < ns * 5) {
+                const int s = threadIdx.x / 5, k = threadIdx.x % 5;
+                const unsigned long long x = s_acc[s][k];
+                if (x) atomicAdd(&sacc[s][k == 4 ? 6 : k], x);
+            }
+            grid_sync(ctr, target, GB);
+
+            // pixels: per-slot accumulators, the point images' cut walks beside
+            // the segment images' sums of squares
+            if (threadIdx.x == 0) {
+                for (int s = 0; s < ns; s++) {
+                    const ulonglong2 a01 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s]));
+                    const unsigned long long a2 = __ldcg(&sacc[s][2]);
+                    Z.mu[s] = ddiv((double)a01.x, (double)M);
+                    Z.fiA[s] = a01.y;
+                    Z.fiB[s] = a2;
+                }
+                if (gb == 0) {
+                    unsigned long long *nxt = &st->sacc[par ^ 1][0][0];
+                    for (int k = 0; k < kSpecK * 8; k++) __stcg(nxt + k, 0ull);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < kPixCutThreads) {
+                for (int p = gb; p < ns * C; p += GB) {
+                    const int s = p / C, cut = p - s * C;
+                    unsigned int *P = img0 + (long long)(3 * s) * M;
+                    const bool mine = local_cuts && cut == gb % C;
+                    const double r = eval_cut(mine ? tree : gtree, mine ? 0 : cut,
+                                              SqU32Clear{{P, Z.mu[s]}}, scratch, a, kBTraceIters,
+                                              kPixCutThreads, NamedBar{1, kPixCutThreads});
+                    if (threadIdx.x == 0) __stcg(tree.cutval + (long long)s * C + cut, r);
+                }
+            } else {
+                const int nt2 = blockDim.x - kPixCutThreads;
+                const long long t2 = gb * (long long)nt2 + (threadIdx.x - kPixCutThreads);
+                const long long s2 = (long long)GB * nt2;
+                __shared__ unsigned long long s_ws[32][2 * kSpecK];
+                const int wid = threadIdx.x >> 5;
+                for (int s = 0; s < ns; s++) {
+                    unsigned int *A = img0 + (long long)(3 * s + 1) * M, *B = A + M;
+                    unsigned long long ws0 = 0, ws1 = 0;
+                    for (long long p = t2; p < M; p += s2) {
+                        const unsigned long long ha = __ldcg(A + p), hb = __ldcg(B + p);
+                        if (ha) { ws0 += ha * ha; A[p] = 0u; }
+                        if (hb) { ws1 += hb * hb; B[p] = 0u; }
+                    }
+                    ws0 = warp_sum(ws0);
+                    ws1 = warp_sum(ws1);
+                    if (lane == 0) { s_ws[wid][2 * s] = ws0; s_ws[wid][2 * s + 1] = ws1; }
+                }
+                asm volatile("bar.sync 2, %0;" ::"r"(nt2) : "memory");
+                if (threadIdx.x < kPixCutThreads + 2 * ns) {
+                    const int k = threadIdx.x - kPixCutThreads;
+                    unsigned long long x = 0;
+                    for (int w2 = kPixCutThreads >> 5; w2 < (int)(blockDim.x >> 5); w2++)
+                        x += s_ws[w2][k];
+                    if (x) atomicAdd(&sacc[k >> 1][4 + (k & 1)], x);
+                }
+            }
+            grid_sync(ctr, target, GB);
+
+            // step: finish every slot's contrast and bounds, then replay the
+            // reference's pops while their results are known
+            for (int i = threadIdx.x; i < ns * C; i += blockDim.x)
+                scratch[(i / C) * (C + ntop) + (i % C)] = __ldcg(tree.cutval + i);
+            __syncthreads();
+            if (C > 1) {
+                const int levels = tree.top_levels;
+                const int4 tr = threadIdx.x < ns * ntop ? tree.top[threadIdx.x % ntop]
+                                                        : make_int4(0, 0, 0, -1);
+                double *vv = scratch + (threadIdx.x / (ntop > 0 ? ntop : 1)) * (C + ntop);
+                if (ns * ntop <= (int)blockDim.x) {
+                    for (int h = 0; h < levels; h++) {
+                        if (tr.w == h) vv[tr.x] = dadd(vv[tr.y], vv[tr.z]);
+                        __syncthreads();
+                    }
+                } else if (threadIdx.x == 0) {
+                    Z.status = kStatusSpecOverflow;  // the host falls back to k_solve
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const double Md = (double)M;
+                for (int s = 0; s < ns; s++) {
+                    const double Sv = scratch[s * (C + ntop) + (C > 1 ? tree.top_root : 0)];
+                    const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
+                    const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
+                    const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
+                    Z.marks += a0 + a23.y;
+                    Z.exact += a6;
+                    const double Cs = ddiv(dadd(0.0, Sv), Md);  // np.sum(...) / M
+                    const double cbA = dsub(ddiv((double)a45.x, Md), __ldg(a.pow2 + Z.fiA[s]));
+                    const double cbB = dsub(ddiv((double)a45.y, Md), __ldg(a.pow2 + Z.fiB[s]));
+                    if (s == 0 && mode == kModeRoot) {
+                        Z.S[0] = Cs;
+                        Z.mu[0] = cbA;  // the root bound
+                        continue;
+                    }
+                    SpecRes &r = Z.cache[Z.cache_head];
+                    r.counter = Z.slot[s].counter;
+                    r.C = Cs;
+                    r.cbA = cbA;
+                    r.cbB = cbB;
+                    if (s == 0) Z.cur = Z.cache_head;
+                    Z.cache_head = (Z.cache_head + 1) % kSpecCache;
+                    if (Z.ncache < kSpecCache) Z.ncache++;
+                }
+                if (Z.status == kStatusSpecOverflow) Z.done = 1;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32 && !Z.done) {
+                // warp 0: the pop loop (lane 0 runs the serial parts)
+                SpecSlot node = Z.slot[0];
+                bool root = mode == kModeRoot;
+                int stop = 0, next_uncached = 0;
+                while (true) {
+                    if (lane == 0) {
+                        if (root) {  // solver.py:92-98
+                            Z.c_hat = Z.S[0];
+                            Z.nu_hat = node.c;
+                            Z.point_evals++;
+                            Z.bound_evals++;
+                            if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
+                                Z.status = kStatusSpecOverflow;
+                                stop = 1;
+                            } else {
+                                frs[Z.fr_n++] = FrontierEntry{Z.mu[0], Z.next_counter++, node.lo,
+                                                              node.hi};
+                            }
+                        } else {  // solver.py:109-119
+                            const SpecRes &r = Z.cache[Z.cur];
+                            Z.point_evals++;
+                            if (r.C >= Z.c_hat) {
+                                Z.nu_hat = node.c;
+                                Z.c_hat = r.C;
+                            }
+                            Z.bound_evals += 2;
+                            const double cbA = r.cbA, cbB = r.cbB;
+                            if (cbA >= Z.c_hat) {
+                                if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
+                                    Z.status = kStatusSpecOverflow;
+                                    stop = 1;
+                                } else {
+                                    frs[Z.fr_n++] = FrontierEntry{cbA, Z.next_counter++, node.lo,
+                                                                  node.c};
+                                }
+                            }
+                            if (!stop && cbB >= Z.c_hat) {
+                                if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
+                                    Z.status = kStatusSpecOverflow;
+                                    stop = 1;
+                                } else {
+                                    frs[Z.fr_n++] = FrontierEntry{cbB, Z.next_counter++, node.c,
+                                                                  node.hi};
+                                }
+                            }
+                            if (!stop && Z.iterations >= a.max_iter) {
+                                Z.status = kStatusIterLimit;
+                                stop = 1;
+                            }
+                        }
+                        if (Z.fr_n > Z.max_fr) Z.max_fr = Z.fr_n;
+                        if (!stop && Z.fr_n == 0) stop = 1;  // every interval pruned
+                    }
+                    stop = __shfl_sync(0xffffffffu, stop, 0);
+                    if (stop) break;
+                    __syncwarp();
+                    const long long bi = spec_argmax(frs, Z.fr_n, [](const FrontierEntry &) {
+                        return false;
+                    });
+                    int hit = -1;
+                    if (lane == 0) {
+                        const FrontierEntry top = frs[bi];
+                        frs[bi] = frs[Z.fr_n - 1];  // swap-remove
+                        Z.fr_n--;
+                        Z.iterations++;
+                        const double gap = dsub(top.bound, Z.c_hat);  // solver.py:105-108
+                        if (gap <= a.gamma || dsub(top.hi, top.lo) < a.min_width) {
+                            Z.bound_gap = (0.0 > gap) ? 0.0 : gap;
+                            stop = 1;
+                        } else {
+                            hit = spec_find(Z, top.counter);
+                            spec_set_slot(a, node, top);
+                            if (hit >= 0) Z.cur = hit;
+                            else next_uncached = 1;
+                        }
+                    }
+                    stop = __shfl_sync(0xffffffffu, stop, 0);
+                    next_uncached = __shfl_sync(0xffffffffu, next_uncached, 0);
+                    if (stop) break;
+                    // the popped node's interval, for the next iteration / round
+                    node.lo = __shfl_sync(0xffffffffu, node.lo, 0);
+                    node.hi = __shfl_sync(0xffffffffu, node.hi, 0);
+                    node.c = __shfl_sync(0xffffffffu, node.c, 0);
+                    node.den_lo = __shfl_sync(0xffffffffu, node.den_lo, 0);
+                    node.den_c = __shfl_sync(0xffffffffu, node.den_c, 0);
+                    node.den_hi = __shfl_sync(0xffffffffu, node.den_hi, 0);
+                    node.counter = __shfl_sync(0xffffffffu, node.counter, 0);
+                    root = false;
+                    if (next_uncached) break;
+                }
+                if (stop) {
+                    if (lane == 0) Z.done = 1;
+                } else {
+                    // next round: the popped node, then the best narrow uncached
+                    // entries of the frontier
+                    if (lane == 0) {
+                        Z.slot[0] = node;
+                        Z.nslot = 1;
+                        Z.mode = kModeNode;
+                    }
+                    __syncwarp();
+                    for (int s = 1; s < K; s++) {
+                        const long long bi = spec_argmax(frs, Z.fr_n, [&](const FrontierEntry &e) {
+                            if (dsub(e.hi, e.lo) > kSpecWidth) return true;
+                            for (int q = 0; q < Z.nslot; q++)
+                                if (Z.slot[q].counter == e.counter) return true;
+                            return spec_find(Z, e.counter) >= 0;
+                        });
+                        if (bi < 0) break;
+                        if (lane == 0) {
+                            spec_set_slot(a, Z.slot[Z.nslot], frs[bi]);
+                            Z.nslot++;
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) Z.parity = par ^ 1;
+                }
+            }
+            __syncthreads();
+        }
+        // speculative slots' point images are summed (and cleared) every round;
+        // segment images are cleared by the pixel phase: nothing is left dirty
+        if (gb == 0 && threadIdx.x == 0) {
+            WindowResult &r = a.res[w];
+            r.nu = Z.nu_hat;
+            r.contrast = Z.c_hat;
+            r.bound_gap = Z.bound_gap;
+            r.iterations = Z.iterations;
+            r.bound_evals = Z.bound_evals;
+            r.point_evals = Z.point_evals;
+            r.max_fr = Z.max_fr;
+            r.marks = Z.marks;
+            r.exact = Z.exact;
+            r.status = Z.status;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 constexpr size_t kBoundSmem = sizeof(WarpQueue) * (kThreads / 32);
 constexpr size_t kSolveSmem = kSolveSmemBytes;
+constexpr size_t kSpecSmem = kRegionA + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry);
 
 static bool g_attrs = false;
 static void set_attrs()
@@ -1416,6 +1832,8 @@ static void set_attrs()
                          (int)kSolveSmem);
     cudaFuncSetAttribute(k_event_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kQueueBytes);
+    cudaFuncSetAttribute(k_solve_spec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSpecSmem);
     g_attrs = true;
 }
 
@@ -1528,6 +1946,15 @@ int solve_grid_blocks(int device)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm < 1) per_sm = 1;
     return per_sm * sms;
+}
+
+cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, cudaStream_t s)
+{
+    set_attrs();
+    SolveArgs args = a;
+    void *params[] = {&args};
+    return cudaLaunchCooperativeKernel((const void *)k_solve_spec, dim3(blocks),
+                                       dim3(kSolveThreads), params, kSpecSmem, s);
 }
 
 cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s)

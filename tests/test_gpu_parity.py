@@ -159,6 +159,27 @@ def test_bnb_both_event_paths(bnb_golden, monkeypatch, path):
         assert _same(r, cfgs[cfg]["result"])
 
 
+@pytest.mark.parametrize("k", ["1", "2", "4"])
+def test_bnb_speculative_rounds(bnb_golden, monkeypatch, k):
+    """Speculative rounds (k_solve_spec, up to k node evaluations per round) and
+    the one-node kernel give the reference's results on every golden window,
+    configs 1-2 and the grouped window solver."""
+    monkeypatch.setenv("EVD_SPEC_K", k)
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        assert _same(evd.maximise_contrast_bnb(batch, evd.SolverParams()), w["result"])
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        gold = json.load(fh)
+    for cfg in ("1", "2"):
+        r, st = sol.solve_window(synth.config_window(int(cfg)), evd.SolverParams())
+        assert _same(r, gold["configs"][cfg]["result"])
+    seq = gold["sequence"]
+    res, _, _ = sol.solve_windows([synth.sequence_window(s["k"]) for s in seq],
+                                  evd.SolverParams(), groups=2)
+    for r, s in zip(res, seq):
+        assert r.status == 0 and _same(r, s["result"])
+
+
 def test_bnb_trace_nodes(bnb_golden):
     """Every node the reference evaluated: centre contrast and both child c_bar bits."""
     meta, windows = bnb_golden
