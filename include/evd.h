@@ -124,6 +124,8 @@ typedef struct {
     double device_ms;     /* device time of the solve (CUDA events on the ctx stream) */
     uint64_t marks;       /* pixel increments made in all images (atomic work) */
     uint64_t exact_events;/* event x node evaluations that needed the exact (division) path */
+    int64_t rounds;       /* device rounds (grid-wide node-evaluation steps): < iterations
+                             when speculative rounds evaluated several nodes at once */
 } evd_solve_result;
 
 /* Whole solve on the device for the resident window (one cooperative
@@ -144,6 +146,7 @@ typedef struct {
     uint64_t marks, exact_events;
     int32_t status;
     int32_t groups;   /* solver groups the launch used */
+    int64_t rounds;   /* device rounds (see evd_solve_result) */
 } evd_window_result;
 
 int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, int32_t groups,

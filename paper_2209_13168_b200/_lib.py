@@ -56,7 +56,8 @@ class SolveResult(ctypes.Structure):
                 ("bound_gap", ctypes.c_double), ("iterations", ctypes.c_int64),
                 ("bound_evals", ctypes.c_int64), ("point_evals", ctypes.c_int64),
                 ("max_frontier", ctypes.c_int64), ("device_ms", ctypes.c_double),
-                ("marks", ctypes.c_uint64), ("exact_events", ctypes.c_uint64)]
+                ("marks", ctypes.c_uint64), ("exact_events", ctypes.c_uint64),
+                ("rounds", ctypes.c_int64)]
 
 
 class WindowResult(ctypes.Structure):
@@ -65,7 +66,8 @@ class WindowResult(ctypes.Structure):
                 ("bound_evals", ctypes.c_int64), ("point_evals", ctypes.c_int64),
                 ("max_frontier", ctypes.c_int64), ("marks", ctypes.c_uint64),
                 ("exact_events", ctypes.c_uint64),
-                ("status", ctypes.c_int32), ("groups", ctypes.c_int32)]
+                ("status", ctypes.c_int32), ("groups", ctypes.c_int32),
+                ("rounds", ctypes.c_int64)]
 
 
 _d = ctypes.POINTER(ctypes.c_double)

@@ -951,6 +951,7 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
     res->max_frontier = w.max_fr;
     res->marks = w.marks;
     res->exact_events = w.exact;
+    res->rounds = w.rounds;
     res->device_ms = ms;
     if (w.status == kStatusIterLimit)
         return fail(ctx, EVD_ERR_ITER_LIMIT,
@@ -990,6 +991,7 @@ static int solve_offsets(evd_ctx *ctx, const long long *offsets, int n_windows, 
         r.max_frontier = out[w].max_fr;
         r.marks = out[w].marks;
         r.exact_events = out[w].exact;
+        r.rounds = out[w].rounds;
         r.status = out[w].status == kStatusOk ? EVD_OK
                    : out[w].status == kStatusIterLimit ? EVD_ERR_ITER_LIMIT
                    : out[w].status == kStatusEmpty ? EVD_ERR_NO_EVENTS : EVD_ERR_CUDA;

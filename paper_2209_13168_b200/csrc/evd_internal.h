@@ -60,7 +60,7 @@ struct WindowResult {
     double nu, contrast, bound_gap;
     long long iterations, bound_evals, point_evals, max_fr;
     unsigned long long marks, exact;
-    int status, pad;
+    int status, rounds;  // rounds: grid-wide node-evaluation steps
 };
 
 struct SolveArgs {

@@ -1394,6 +1394,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveAr
             r.marks = R.marks;
             r.exact = R.exact;
             r.status = R.status;
+            r.rounds = (int)R.point_evals;  // one node evaluation per round
         }
     }
 }
@@ -1432,6 +1433,7 @@ struct SpecState {
     SpecRes cache[kSpecCache];
     int ncache, cache_head;
     int cur;  // cache index of the node being processed (-1: slot results below)
+    int rounds;
 };
 
 __device__ __forceinline__ int spec_find(const SpecState &Z, long long counter)
@@ -1536,6 +1538,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(So
             Z.iterations = Z.bound_evals = Z.point_evals = Z.next_counter = Z.fr_n = Z.max_fr = 0;
             Z.marks = Z.exact = 0;
             Z.ncache = Z.cache_head = 0;
+            Z.rounds = 0;
         }
         __syncthreads();
         while (!Z.done) {
@@ -1647,6 +1650,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(So
             __syncthreads();
             if (threadIdx.x == 0) {
                 const double Md = (double)M;
+                Z.rounds++;
                 for (int s = 0; s < ns; s++) {
                     const double Sv = scratch[s * (C + ntop) + (C > 1 ? tree.top_root : 0)];
                     const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
@@ -1809,6 +1813,7 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(So
             r.marks = Z.marks;
             r.exact = Z.exact;
             r.status = Z.status;
+            r.rounds = Z.rounds;
         }
     }
 }
