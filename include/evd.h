@@ -56,7 +56,10 @@ int evd_device_sms(const evd_ctx *ctx);
 
 /* ---- event window (EventBatch, events.py:93-120) ---------------------- */
 /* Copies one window's SoA events (x, y, t in [0, tau]) to device memory; they
- * stay resident for every following evaluation until the next call. */
+ * stay resident for every following evaluation until the next call.  The
+ * arrays may be host memory or device memory of the context's GPU (unified
+ * addressing): a window broadcast to every rank's GPU (NCCL) is loaded without
+ * a host round trip.  Likewise for evd_solve_stream / evd_load_stream. */
 int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
                    int32_t width, int32_t height, double tau);
 

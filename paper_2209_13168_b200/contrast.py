@@ -66,6 +66,20 @@ def load_window(batch: EventBatch, ctx=None):
     return ctx
 
 
+def load_window_device(x, y, t, tau: float, geometry, ctx=None):
+    """evd_set_events from device arrays on the context's GPU (torch CUDA
+    tensors of float64, contiguous), e.g. a window broadcast over NCCL."""
+    import ctypes
+    ctx = ctx or _lib.context()
+    n = int(t.numel())
+    ptr = lambda v: ctypes.cast(ctypes.c_void_p(v.data_ptr()), _lib._d)
+    rc = ctx.lib.evd_set_events(ctx.h, ptr(x), ptr(y), ptr(t), n, geometry.width,
+                                geometry.height, float(tau))
+    if rc:
+        _raise(ctx, rc)
+    return ctx
+
+
 def point_terms(batch: EventBatch, nus, images: bool = False, ctx=None, loaded=False,
                 with_contrast: bool = True):
     """accumulate_image + image_contrast at every nu in ``nus`` on the device.

@@ -501,9 +501,9 @@ int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double 
     CU(ctx->t.ensure(n));
     if (n > 0) {
         // raw x, y land in the centred buffers and are centred in place
-        CU(cudaMemcpyAsync(ctx->xc.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->yc.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->t.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->xc.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->yc.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->t.p, t, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
         launch_center(ctx->xc.p, ctx->yc.p, n, width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p,
                       ctx->stream);
         LAUNCHED(1);
@@ -1098,9 +1098,9 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
     CU(ctx->sy.ensure(std::max(n, (int64_t)1)));
     CU(ctx->st.ensure(std::max(n, (int64_t)1)));
     if (n > 0) {
-        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
     }
     ctx->sn = n;
     ctx->sW = width;
@@ -1203,9 +1203,9 @@ int evd_load_stream(evd_ctx *ctx, const double *x, const double *y, const double
     CU(ctx->st.ensure(m));
     CU(ctx->sp.ensure(m));
     if (n > 0) {
-        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
         if (p) CU(cudaMemcpyAsync(ctx->sp.p, p, n, cudaMemcpyHostToDevice, ctx->stream));
     }
     ctx->sn = n;

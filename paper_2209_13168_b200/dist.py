@@ -11,9 +11,12 @@ shards naturally.
   children in one pass, and keeps the reference's incumbent (>=) and pruning
   (>=) rules.  With a process group the round's evaluations are split over
   the ranks (events replicated on every GPU: S_bar is not additive over event
-  shards) and their integers all-gathered, so every rank holds the identical
-  BnB state.  Certified within gamma of the global optimum like the reference
-  (SURVEY §8(c) parity P3).
+  shards) and their results all-gathered (one small tensor per round), so
+  every rank holds the identical BnB state.  Certified within gamma of the
+  global optimum like the reference (SURVEY §8(c) parity P3).
+* ``broadcast_window`` / ``solve_batched_dist`` -- the window's events go from
+  one rank to every GPU once (one packed float64 tensor, NCCL broadcast over
+  NVLink) and are loaded into each rank's libevd context from device memory.
 
 The evaluators are injectable so the host logic runs under ``gloo`` on CPU
 (tests/test_dist.py); on GPUs they default to the libevd entry points.
@@ -85,12 +88,12 @@ class BatchedResult:
     bound_evals: int     # bound evaluations incl. the root
 
 
-def gpu_evaluators(batch):
+def gpu_evaluators(batch, ctx=None):
     """(centres -> contrasts, (lo, hi) -> c_bar) on this process's GPU; the
-    window is loaded once."""
+    window is loaded once (or is already resident in ``ctx``)."""
     from .contrast import assemble_bound, frontier_terms, load_window, point_terms
 
-    ctx = load_window(batch)
+    ctx = ctx if ctx is not None else load_window(batch)
     m = batch.geometry.n_pixels
 
     def contrasts(nus):
@@ -103,9 +106,20 @@ def gpu_evaluators(batch):
     return contrasts, bounds
 
 
+def _coll_device(group):
+    """Tensor device for collectives: the rank's GPU under NCCL, else the CPU."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def _split_eval(fn, args, group):
     """Evaluate fn over the items of ``args`` split round-robin over the ranks
-    and all-gather the results (identical arrays on every rank)."""
+    and all-gather the results (identical arrays on every rank): one padded
+    float64 tensor per rank, all-gathered over the group's backend."""
+    import torch
     import torch.distributed as dist
 
     if group is None and not dist.is_initialized():
@@ -115,12 +129,58 @@ def _split_eval(fn, args, group):
     mine = np.arange(rank, n, world)
     vals = np.asarray(fn(*[np.asarray(a)[mine] for a in args]), dtype=np.float64) if len(mine) else \
         np.empty(0)
-    parts = [None] * world
-    dist.all_gather_object(parts, vals.tolist(), group=group)
+    width = -(-n // world)  # ceil: rank r holds items r, r + world, ...
+    dev = _coll_device(group)
+    local = torch.zeros(width, dtype=torch.float64, device=dev)
+    local[: len(vals)] = torch.from_numpy(vals).to(dev)
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local, group=group)
     out = np.empty(n, dtype=np.float64)
     for r, part in enumerate(parts):
-        out[np.arange(r, n, world)] = part
+        idx = np.arange(r, n, world)
+        out[idx] = part[: len(idx)].cpu().numpy()
     return out
+
+
+def broadcast_window(batch, group=None, src: int = 0):
+    """The window's events from rank ``src`` to every rank: one
+    packed float64 tensor [x | y | t] broadcast over the group's backend (NCCL:
+    GPU to GPU over NVLink).  Ranks other than ``src`` pass ``batch=None``.
+    Returns (x, y, t, tau, geometry), tensors on the collective device."""
+    import torch
+    import torch.distributed as dist
+
+    from .events import SensorGeometry
+    dev = _coll_device(group)
+    rank = dist.get_rank(group)
+    meta = torch.zeros(4, dtype=torch.float64, device=dev)
+    if rank == src:
+        g = batch.geometry
+        meta[:] = torch.tensor([batch.n, g.width, g.height, float(batch.tau)], dtype=torch.float64)
+    dist.broadcast(meta, src=src, group=group)
+    n, w, h, tau = int(meta[0]), int(meta[1]), int(meta[2]), float(meta[3])
+    buf = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    if rank == src:
+        host = np.concatenate([np.asarray(batch.x, np.float64), np.asarray(batch.y, np.float64),
+                               np.asarray(batch.t, np.float64)])
+        buf.copy_(torch.from_numpy(host))
+    dist.broadcast(buf, src=src, group=group)
+    return buf[:n], buf[n:2 * n], buf[2 * n:], tau, SensorGeometry(w, h)
+
+
+def solve_batched_dist(batch, params, k: int = 64, group=None, src: int = 0) -> "BatchedResult":
+    """``solve_batched`` over the ranks of ``group`` on GPUs: events broadcast
+    once from ``src`` and loaded from device memory, each round's evaluations
+    split over the ranks.  Every rank returns the identical result."""
+    from types import SimpleNamespace
+
+    from .contrast import load_window_device
+    x, y, t, tau, geometry = broadcast_window(batch, group, src)
+    ctx = load_window_device(x, y, t, tau, geometry)
+    view = SimpleNamespace(n=int(t.numel()), tau=tau, geometry=geometry)
+    contrasts, bounds = gpu_evaluators(view, ctx=ctx)
+    return solve_batched(view, params, k=k, contrasts=contrasts, bounds=bounds, group=group,
+                         split=True)
 
 
 def solve_batched(batch, params, k: int = 64, contrasts: Callable | None = None,

@@ -63,8 +63,12 @@ def _worker(rank, world, port, queue):
         b = wins[1]
         c, bd = _oracle_evaluators(b)
         res = pdist.solve_batched(b, params, k=8, contrasts=c, bounds=bd, split=True)
+        # the window's events from rank 0 to every rank (one packed broadcast)
+        x, y, t, tau, geom = pdist.broadcast_window(b if rank == 0 else None)
+        same = (np.array_equal(x.numpy(), b.x) and np.array_equal(y.numpy(), b.y) and
+                np.array_equal(t.numpy(), b.t) and tau == b.tau and geom == b.geometry)
         queue.put((rank, [(s.t, s.contrast, s.iterations) for s in samples],
-                   (res.nu, res.contrast, res.rounds, res.nodes)))
+                   (res.nu, res.contrast, res.rounds, res.nodes), same))
     finally:
         dist.destroy_process_group()
 
@@ -90,10 +94,11 @@ def test_world2_gloo_windows_and_split_frontier():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    outs.sort()
-    (_, s0, r0), (_, s1, r1) = outs
+    outs.sort(key=lambda o: o[0])
+    (_, s0, r0, b0), (_, s1, r1, b1) = outs
     # both ranks hold the full, identical sample list and the identical BnB state
     assert s0 == s1 and r0 == r1
+    assert b0 and b1  # the broadcast window equals the source batch on both ranks
     serial = _oracle_stream(_windows(), SolverParams())
     assert s0 == [(s.t, s.contrast, s.iterations) for s in serial]
     # the split batched solve equals the single-process batched solve ...

@@ -78,3 +78,28 @@ def test_batched_frontier_bnb_within_gamma(cfg, k):
     assert r.rounds < ref["iterations"]
     # the incumbent is a real contrast value of the reference objective
     assert r.contrast == evd.contrast_at(b, r.nu)
+
+
+def test_dist_batched_over_nccl_world1():
+    """The multi-GPU frontier path on one GPU: events broadcast over NCCL and
+    loaded from device memory, results gathered as tensors; equals the
+    single-process batched solve."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2209_13168_b200 import dist as pdist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        b = synth.config_window(1)
+        got = pdist.solve_batched_dist(b, evd.SolverParams(), k=16)
+    finally:
+        dist.destroy_process_group()
+    ref = pdist.solve_batched(b, evd.SolverParams(), k=16)
+    assert (got.nu, got.contrast, got.bound_gap, got.rounds, got.nodes) == (
+        ref.nu, ref.contrast, ref.bound_gap, ref.rounds, ref.nodes)
