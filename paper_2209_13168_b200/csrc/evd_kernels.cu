@@ -5,6 +5,7 @@
 // radial_warp); k_solve is the device-resident branch and bound
 // (solver.py:79-123) that evaluates one node per grid-wide step.
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 
 #include "evd_device.cuh"
@@ -355,6 +356,123 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
             warp_drain_list(wq, nq, W, H);
             nq = 0;
         }
+    }
+    if (nq > 0) {
+        __syncwarp();
+        warp_drain_list(wq, nq, W, H);
+    }
+    if (valid && fi) atomicAdd(s_fi + lane, fi);
+    __syncthreads();
+    if (threadIdx.x < kFrontGroup && g * kFrontGroup + (int)threadIdx.x < K) {
+        const int kk = g * kFrontGroup + threadIdx.x;
+        if (s_fi[threadIdx.x]) atomicAdd(fi_out + kk, s_fi[threadIdx.x]);
+    }
+}
+
+// k_frontier with a filtered first pass: each (event, interval) segment is
+// warped with one multiplication by RN(1/den) and certified against a rounding
+// margin (sure_segment: off-frame, or both endpoints surely in one pixel);
+// the rest -- segments near pixel edges or crossing them -- are queued per
+// warp as (event, interval) pairs and take the exact path 32 at a time with
+// full lanes.  Same images and counts as k_frontier (every certified result
+// is what the exact arithmetic gives).
+__global__ void __launch_bounds__(kThreads) k_frontier_f(
+    const double *__restrict__ xc, const double *__restrict__ yc, const double *__restrict__ t,
+    long long n, const double *__restrict__ lo, const double *__restrict__ hi,
+    const double *__restrict__ den_lo, const double *__restrict__ den_hi, int K, double cx,
+    double cy, int W, int H, unsigned int *images, long long M, int bpg,
+    unsigned long long *fi_out)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
+    __shared__ unsigned long long s_fi[kFrontGroup];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int g = blockIdx.x / bpg, tb = blockIdx.x % bpg;
+    const int k = g * kFrontGroup + lane;
+    const bool valid = k < K;
+    const int kc = valid ? k : K - 1;
+    const double my_lo = __ldg(lo + kc), my_hi = __ldg(hi + kc);
+    const double my_dlo = __ldg(den_lo + kc), my_dhi = __ldg(den_hi + kc);
+    const double my_rlo = ddiv(1.0, my_dlo), my_rhi = ddiv(1.0, my_dhi);
+    const double left_hi = __shfl_up_sync(0xffffffffu, my_hi, 1);
+    const bool shared_lo = lane > 0 && my_lo == left_hi;
+    unsigned int *img = images + (long long)kc * M;
+    AtomicSink sink{img};
+    if (threadIdx.x < kFrontGroup) s_fi[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long fi = 0;
+    int nq = 0;  // segments pooled in wq.d (warp-uniform)
+    int nx = 0;  // uncertain (event, interval) pairs queued in wq.ev (warp-uniform)
+    // the exact path for the last `take` queued pairs, with full lanes
+    auto exact_batch = [&](int take) {
+        const long long code = lane < take ? wq.ev[nx - take + lane] : -1;
+        nx -= take;
+        __syncwarp();
+        const int j = code >= 0 ? (int)(code & 31) : 0;
+        const double lo_j = __shfl_sync(0xffffffffu, my_lo, j);
+        const double hi_j = __shfl_sync(0xffffffffu, my_hi, j);
+        const double dlo_j = __shfl_sync(0xffffffffu, my_dlo, j);
+        const double dhi_j = __shfl_sync(0xffffffffu, my_dhi, j);
+        AtomicSink sj{images + (long long)(g * kFrontGroup + j) * M};
+        SegDesc d;
+        int c = 0, m = 0;
+        if (code >= 0) {
+            const long long e = code >> 5;
+            const double x = __ldg(xc + e), y = __ldg(yc + e), tt = __ldg(t + e);
+            const Warped a = warp_event(x, y, tt, lo_j, dlo_j, cx, cy);
+            const Warped b = warp_event(x, y, tt, hi_j, dhi_j, cx, cy);
+            const int ins = fully_inside(a.x, a.y, b.x, b.y, W, H);
+            if (ins) atomicAdd(s_fi + j, (unsigned long long)ins);
+            c = build_segment(a.x, a.y, b.x, b.y, W, H, kChunk, d, sj, m);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
+        if (c > 0) {
+            const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+            wq.d[slot] = d;
+            wq.img[slot] = sj.img;
+        }
+        nq += __popc(bal);
+        if (nq >= 32) {
+            __syncwarp();
+            warp_drain_list(wq, nq, W, H);
+            nq = 0;
+        }
+    };
+    const long long gw = (long long)tb * wpb + warp, nw = (long long)bpg * wpb;
+    for (long long e = gw; e < n; e += nw) {
+        const double x = __ldg(xc + e), y = __ldg(yc + e), tt = __ldg(t + e);
+        const Warped bq = warp_approx(x, y, tt, my_hi, my_rhi, cx, cy);
+        const double mb = sure_margin(bq, cx, cy);
+        Warped aq;
+        aq.x = __shfl_up_sync(0xffffffffu, bq.x, 1);
+        aq.y = __shfl_up_sync(0xffffffffu, bq.y, 1);
+        double ma = __shfl_up_sync(0xffffffffu, mb, 1);
+        if (!shared_lo) {
+            aq = warp_approx(x, y, tt, my_lo, my_rlo, cx, cy);
+            ma = sure_margin(aq, cx, cy);
+        }
+        bool unc = false;
+        if (valid) {
+            long long pix;
+            int ins;
+            if (sure_segment(aq, bq, ma, mb, W, H, pix, ins)) {
+                if (pix >= 0) sink(pix);
+                fi += ins;
+            } else {
+                unc = true;
+            }
+        }
+        const unsigned bu = __ballot_sync(0xffffffffu, unc);
+        if (unc) wq.ev[nx + __popc(bu & ((1u << lane) - 1u))] = e * 32 + lane;
+        nx += __popc(bu);
+        if (nx >= 32) {
+            __syncwarp();
+            exact_batch(32);
+        }
+    }
+    while (nx > 0) {
+        __syncwarp();
+        exact_batch(nx < 32 ? nx : 32);
     }
     if (nq > 0) {
         __syncwarp();
@@ -1831,6 +1949,8 @@ static void set_attrs()
                          (int)kBoundSmem);
     cudaFuncSetAttribute(k_frontier, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBoundSmem);
+    cudaFuncSetAttribute(k_frontier_f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBoundSmem);
     cudaFuncSetAttribute(k_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSolveSmem);
     cudaFuncSetAttribute(k_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1888,8 +2008,13 @@ void launch_frontier(const double *xc, const double *yc, const double *t, long l
     long long bpg = (n + kThreads - 1) / kThreads;
     if (bpg > (long long)num_sms() * 4) bpg = (long long)num_sms() * 4;
     if (bpg < 1) bpg = 1;
-    k_frontier<<<(unsigned)(groups * bpg), kThreads, kBoundSmem, s>>>(
-        xc, yc, t, n, lo, hi, den_lo, den_hi, K, cx, cy, W, H, images, M, (int)bpg, fi_out);
+    static const bool exact_only = getenv("EVD_FRONTIER_FILTER") && getenv("EVD_FRONTIER_FILTER")[0] == '0';
+    if (exact_only)
+        k_frontier<<<(unsigned)(groups * bpg), kThreads, kBoundSmem, s>>>(
+            xc, yc, t, n, lo, hi, den_lo, den_hi, K, cx, cy, W, H, images, M, (int)bpg, fi_out);
+    else
+        k_frontier_f<<<(unsigned)(groups * bpg), kThreads, kBoundSmem, s>>>(
+            xc, yc, t, n, lo, hi, den_lo, den_hi, K, cx, cy, W, H, images, M, (int)bpg, fi_out);
     long long bpi = (M + kThreads * 4 - 1) / (kThreads * 4);
     if (bpi < 1) bpi = 1;
     k_frontier_sums<<<(unsigned)(K * bpi), kThreads, 0, s>>>(images, M, (int)bpi, marks_s);
