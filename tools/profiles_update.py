@@ -58,6 +58,15 @@ def main():
     with open(os.path.join(PR, f"probe_events_{tag}.txt"), "w") as fh:
         for c in (2, 3):
             fh.write(open(os.path.join(EV, f"probe_cfg{c}.txt")).read())
+    frep = os.path.join(EV, "k_frontier_cfg3.ncu-rep")
+    if os.path.exists(frep):
+        raw = subprocess.run(["ncu", "-i", frep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout.splitlines()
+        rows = list(csv.reader(raw))
+        h, u, v = rows[0], rows[1], rows[2]
+        fout = {k: [v[h.index(k)], u[h.index(k)]] for k in WANT if k in h}
+        with open(os.path.join(PR, f"ncu_k_frontier_cfg3_{tag}.json"), "w") as fh:
+            json.dump(fout, fh, indent=1)
     print(json.dumps(out, indent=0)[:800])
 
 

@@ -16,3 +16,6 @@ ncu --set full --import-source on --clock-control none -k regex:k_solve -c 1 -f 
     -o gpurun_out/ev/k_solve_cfg2 python bench.py --steps 1 --warmup 3 --no-cpu --no-extra \
     > gpurun_out/ev/ncu_full.log 2>&1
 tail -2 gpurun_out/ev/ncu_full.log
+python tools/bench_frontier.py 1 > /dev/null 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:k_frontier_f -c 1 -f \
+    -o gpurun_out/ev/k_frontier_cfg3 python tools/bench_frontier.py 1 > gpurun_out/ev/ncu_frontier.log 2>&1
