@@ -797,6 +797,8 @@ namespace {
 // off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
 constexpr long long kFilterMinEvents = LLONG_MAX;
 constexpr long long kSpecMaxEvents = 500000;  // speculative rounds for windows below this
+constexpr long long kSmallWindow = 100000;    // 384-thread CTAs below this (whole grid)
+constexpr long long kLargeWindow = 500000;    // 768-thread CTAs from this on (whole grid)
 
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
@@ -827,6 +829,14 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? 2 : 1;
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
     if (ctx->trace_on) spec_k = 1;
+    // CTA size: small windows on the whole grid are latency-bound (384 fatter
+    // threads), large ones sampler-throughput-bound (768); grouped solves and
+    // the traced build stay at 512 (measured: cfg 1 1.10 -> 1.04 ms at 384,
+    // cfg 3 21.5 -> 20.3 ms at 768, cfg 2 and cfg 4 best at 512)
+    int threads = 512;
+    if (GB >= 32 && !ctx->trace_on)
+        threads = max_n < kSmallWindow ? 384 : (max_n >= kLargeWindow ? 768 : 512);
+    if (const char *e = getenv("EVD_SOLVE_BLOCK")) threads = atoi(e);
     if ((rc = ensure_pow2(ctx, M, max_n))) return rc;
     if (ctx->simg.cap < (size_t)(3 * kSpecK * M * groups)) {  // the kernels leave them zeroed
         CU(ctx->simg.ensure((size_t)(3 * kSpecK * M * groups)));
@@ -896,8 +906,9 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         a.spec_k = spec_k;
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU((spec_k > 1 || getenv("EVD_SPEC_FORCE")) ? launch_solve_spec(a, groups * GB, ctx->stream)
-                      : launch_solve(a, groups * GB, ctx->stream));
+        CU((spec_k > 1 || getenv("EVD_SPEC_FORCE"))
+               ? launch_solve_spec(a, groups * GB, threads, ctx->stream)
+               : launch_solve(a, groups * GB, threads, ctx->stream));
         LAUNCHED(1);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
         std::vector<WindowResult> got(n_windows);

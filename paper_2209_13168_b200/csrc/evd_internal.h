@@ -142,8 +142,9 @@ void launch_raster_segments(const double *segs, int k, int W, int H, int chunk, 
                             cudaStream_t s);
 int solve_grid_blocks(int device);
 int solve_block_threads();
-cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s);
-cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, cudaStream_t s);
+// threads per CTA: 384, 512 or 768 (anything else runs at 512)
+cudaError_t launch_solve(const SolveArgs &a, int blocks, int threads, cudaStream_t s);
+cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, int threads, cudaStream_t s);
 cudaError_t decode_bin(const unsigned char *body_dev, long long n, int W, int H, double *x,
                        double *y, double *t, signed char *p, void *scratch, size_t scratch_bytes,
                        unsigned int *flags_dev, unsigned int *flags_host, int *launches,

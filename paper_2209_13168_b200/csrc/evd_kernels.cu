@@ -1190,12 +1190,18 @@ __device__ double top_combine(const TreeDev &T, double *v)
 
 constexpr size_t kQueueBytes = sizeof(WarpQueue) * (kSolveThreads / 32);
 constexpr size_t kStepBytes = kCutSmem * sizeof(double) + kFrView * sizeof(FrontierEntry);
-constexpr size_t kRegionA = kQueueBytes > kStepBytes ? kQueueBytes : kStepBytes;
-constexpr size_t kSolveSmemBytes = kRegionA + sizeof(TreeCache);
+// dynamic shared memory of the solve kernels at NT threads per CTA: region A
+// (warp queues | cut scratch + frontier view), then the cached cut plan
+template <int NT>
+struct SolveSmem {
+    static constexpr size_t queue = sizeof(WarpQueue) * (NT / 32);
+    static constexpr size_t region_a = queue > kStepBytes ? queue : kStepBytes;
+};
 
-template <bool FILTER>
-__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve(SolveArgs a_param)
+template <bool FILTER, int NT>
+__global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 {
+    constexpr size_t kRegionA = SolveSmem<NT>::region_a;
     extern __shared__ __align__(16) unsigned char smem[];
 #ifdef EVD_ARGS_SMEM
     __shared__ SolveArgs a_s;
@@ -1595,8 +1601,10 @@ __device__ __forceinline__ void spec_set_slot(const SolveArgs &a, SpecSlot &s,
     s.counter = e.counter;
 }
 
-__global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(SolveArgs a)
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
 {
+    constexpr size_t kRegionA = SolveSmem<NT>::region_a;
     extern __shared__ __align__(16) unsigned char smem[];
     WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
     double *scratch = reinterpret_cast<double *>(smem);
@@ -1938,8 +1946,13 @@ __global__ void __launch_bounds__(kSolveThreads, EVD_SOLVE_MINB) k_solve_spec(So
 
 // ---------------------------------------------------------------- launchers
 constexpr size_t kBoundSmem = sizeof(WarpQueue) * (kThreads / 32);
-constexpr size_t kSolveSmem = kSolveSmemBytes;
-constexpr size_t kSpecSmem = kRegionA + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry);
+template <int NT>
+constexpr size_t solve_smem() { return SolveSmem<NT>::region_a + sizeof(TreeCache); }
+template <int NT>
+constexpr size_t spec_smem()
+{
+    return SolveSmem<NT>::region_a + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry);
+}
 
 static bool g_attrs = false;
 static void set_attrs()
@@ -1951,14 +1964,22 @@ static void set_attrs()
                          (int)kBoundSmem);
     cudaFuncSetAttribute(k_frontier_f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBoundSmem);
-    cudaFuncSetAttribute(k_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSolveSmem);
-    cudaFuncSetAttribute(k_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSolveSmem);
+    cudaFuncSetAttribute(k_solve<false, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)solve_smem<384>());
+    cudaFuncSetAttribute(k_solve<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)solve_smem<512>());
+    cudaFuncSetAttribute(k_solve<false, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)solve_smem<768>());
+    cudaFuncSetAttribute(k_solve<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)solve_smem<512>());
     cudaFuncSetAttribute(k_event_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kQueueBytes);
-    cudaFuncSetAttribute(k_solve_spec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSpecSmem);
+    cudaFuncSetAttribute(k_solve_spec<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)spec_smem<384>());
+    cudaFuncSetAttribute(k_solve_spec<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)spec_smem<512>());
+    cudaFuncSetAttribute(k_solve_spec<768>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)spec_smem<768>());
     g_attrs = true;
 }
 
@@ -2071,32 +2092,45 @@ int solve_grid_blocks(int device)
 {
     set_attrs();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<true>, kSolveThreads, kSolveSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<true, 512>, 512,
+                                                  solve_smem<512>());
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm < 1) per_sm = 1;
     return per_sm * sms;
 }
 
-cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, cudaStream_t s)
+// One CTA per SM at every block size (128 registers at 512 threads, 168 at
+// 384, 85 at 768): fewer, fatter threads suit latency-bound small windows,
+// more threads the sampler throughput of large ones (solve_threads_for).
+cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, int threads, cudaStream_t s)
 {
     set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
-    return cudaLaunchCooperativeKernel((const void *)k_solve_spec, dim3(blocks),
-                                       dim3(kSolveThreads), params, kSpecSmem, s);
+    const void *fn = threads == 384 ? (const void *)k_solve_spec<384>
+                   : threads == 768 ? (const void *)k_solve_spec<768>
+                                    : (const void *)k_solve_spec<512>;
+    const size_t smem = threads == 384 ? spec_smem<384>()
+                      : threads == 768 ? spec_smem<768>() : spec_smem<512>();
+    if (threads != 384 && threads != 768) threads = 512;
+    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(threads), params, smem, s);
 }
 
-cudaError_t launch_solve(const SolveArgs &a, int blocks, cudaStream_t s)
+cudaError_t launch_solve(const SolveArgs &a, int blocks, int threads, cudaStream_t s)
 {
     set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
-    // the filtered path (approximate warps, exact fallback) pays off for large
-    // windows; small ones keep the leaner exact-only event loop
-    const void *fn = a.filter ? (const void *)k_solve<true> : (const void *)k_solve<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kSolveThreads),
-                                       params, kSolveSmem, s);
+    // the filtered path (opt-in) is built at 512 threads only
+    if (a.filter || (threads != 384 && threads != 768)) threads = 512;
+    const void *fn = a.filter         ? (const void *)k_solve<true, 512>
+                   : threads == 384   ? (const void *)k_solve<false, 384>
+                   : threads == 768   ? (const void *)k_solve<false, 768>
+                                      : (const void *)k_solve<false, 512>;
+    const size_t smem = threads == 384 ? solve_smem<384>()
+                      : threads == 768 ? solve_smem<768>() : solve_smem<512>();
+    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(threads), params, smem, s);
 }
 
 }  // namespace evd

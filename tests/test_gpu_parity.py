@@ -180,6 +180,23 @@ def test_bnb_speculative_rounds(bnb_golden, monkeypatch, k):
         assert r.status == 0 and _same(r, s["result"])
 
 
+@pytest.mark.parametrize("block", ["384", "512", "768"])
+@pytest.mark.parametrize("k", ["1", "2"])
+def test_bnb_every_block_size(bnb_golden, monkeypatch, block, k):
+    """Each CTA size the solve kernels are built at (384 / 512 / 768 threads,
+    with and without speculative rounds) gives the reference's results."""
+    monkeypatch.setenv("EVD_SOLVE_BLOCK", block)
+    monkeypatch.setenv("EVD_SPEC_K", k)
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        assert _same(evd.maximise_contrast_bnb(batch, evd.SolverParams()), w["result"])
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        gold = json.load(fh)
+    for cfg in ("1", "2"):
+        r, st = sol.solve_window(synth.config_window(int(cfg)), evd.SolverParams())
+        assert _same(r, gold["configs"][cfg]["result"])
+
+
 def test_bnb_trace_nodes(bnb_golden):
     """Every node the reference evaluated: centre contrast and both child c_bar bits."""
     meta, windows = bnb_golden
