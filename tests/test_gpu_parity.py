@@ -239,6 +239,16 @@ def test_bnb_config3_if_golden():
     assert _same(r, ref["result"])
 
 
+def test_bnb_config5_vs_reference():
+    """Config 5 (1280x720, 5.33 M events; 768-thread CTAs): the reference's own
+    result, measured once in this container (BASELINE.md, 1,791 s on one
+    core): nu_hat, C(nu_hat) and the gap bit for bit, 144 iterations."""
+    b = synth.config_window(5)
+    r = evd.maximise_contrast_bnb(b, evd.SolverParams())
+    assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (
+        -0.4000001722040176, 753.9103765755924, 0.015945095486131322, 144)
+
+
 def test_sequence_windows(bnb_golden):
     meta, _ = bnb_golden
     for s in meta["sequence"]:
