@@ -6,6 +6,7 @@
 // (solver.py:79-123) that evaluates one node per grid-wide step.
 #include <cfloat>
 #include <cstdlib>
+#include <atomic>
 #include <climits>
 
 #include "evd_device.cuh"
@@ -40,19 +41,17 @@ constexpr int kPixCutThreads = EVD_PIX_CUT_THREADS;  // pixel phase: threads wal
 #ifndef EVD_GUIDED_WIDTH
 #define EVD_GUIDED_WIDTH (1.0 / 16)
 #endif
-constexpr double kGuidedWidth = EVD_GUIDED_WIDTH;  // nodes wider than this claim guided batches  // sample items per supercover chunk
+constexpr double kGuidedWidth = EVD_GUIDED_WIDTH;  // nodes wider than this claim guided batches
 constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
 
-static int g_num_sms = 0;
+// SM count of the current device (contexts on several devices may share a
+// process, one host thread each)
 static int num_sms()
 {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
 }
 
 static int event_blocks(long long n)
@@ -1954,10 +1953,15 @@ constexpr size_t spec_smem()
     return SolveSmem<NT>::region_a + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry);
 }
 
-static bool g_attrs = false;
+// Kernel attributes are per device: set them once for each device a context
+// launches on (idempotent, so two threads racing on one device is harmless).
+static std::atomic<unsigned long long> g_attrs{0};
 static void set_attrs()
 {
-    if (g_attrs) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (g_attrs.load(std::memory_order_acquire) & bit) return;
     cudaFuncSetAttribute(k_bound_image, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBoundSmem);
     cudaFuncSetAttribute(k_frontier, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1980,7 +1984,7 @@ static void set_attrs()
                          (int)spec_smem<512>());
     cudaFuncSetAttribute(k_solve_spec<768>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)spec_smem<768>());
-    g_attrs = true;
+    g_attrs.fetch_or(bit, std::memory_order_release);
 }
 
 void launch_center(const double *x, const double *y, long long n, double cx, double cy,
