@@ -331,6 +331,22 @@ def run_gpu(args, rank, world, local):
             atomic = {"achieved": ach, "peak": apk, "unit": "G atomics/s",
                       "frac": ach / apk if apk else None, "marks_per_solve": int(res.marks),
                       "peak_source": "tools/bench_atomics.cu (u32 RED, random pixels, M=89960)"}
+        # what does bound the kernel: issue and occupancy from the committed
+        # ncu --set full capture of this launch (profiles/, tools/round_evidence.sh)
+        limiter = None
+        nfile = os.path.join(ROOT, "profiles", "ncu_k_solve_cfg2_r01.json")
+        if os.path.exists(nfile):
+            with open(nfile) as fh:
+                nc = json.load(fh)
+            g = lambda k: float(nc[k][0]) if k in nc else None
+            limiter = {
+                "kind": "latency / issue (sequential BnB rounds; per-warp dependent chains)",
+                "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_pct": g("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                "threads_per_warp_inst": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
+                "registers_per_thread": g("launch__registers_per_thread"),
+                "source": "profiles/ncu_k_solve_cfg2_r01.json"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
@@ -344,6 +360,7 @@ def run_gpu(args, rank, world, local):
                       "marks": int(res.marks), "kernel_ms": k_ms,
                       "device_rounds": int(res.rounds)},
             "atomic_roofline": atomic,
+            "limiter": limiter,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n,
                     "d2h_bytes_per_step": 272},  # SolveState read back (evd_internal.h)
             "gpu_launches": launches,
