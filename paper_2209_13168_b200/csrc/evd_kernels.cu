@@ -34,7 +34,10 @@ constexpr int kChunk = EVD_CHUNK;
 #ifndef EVD_PIX_CUT_THREADS
 #define EVD_PIX_CUT_THREADS 128
 #endif
-constexpr int kPixCutThreads = EVD_PIX_CUT_THREADS;  // pixel phase: threads walking the point image's cut
+// pixel phase: threads walking the point image's cut (the rest sum the
+// segment images), by CTA size: 256 of 768 measured best for large windows
+template <int NT>
+constexpr int pix_cut_threads() { return NT >= 768 ? 2 * EVD_PIX_CUT_THREADS : EVD_PIX_CUT_THREADS; }
 #ifndef EVD_BATCH_DIV
 #define EVD_BATCH_DIV 1
 #endif
@@ -1201,6 +1204,7 @@ template <bool FILTER, int NT>
 __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 {
     constexpr size_t kRegionA = SolveSmem<NT>::region_a;
+    constexpr int kPixCutThreads = pix_cut_threads<NT>();
     extern __shared__ __align__(16) unsigned char smem[];
 #ifdef EVD_ARGS_SMEM
     __shared__ SolveArgs a_s;
@@ -1534,7 +1538,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 // ~3.5x less often.  The frontier is replicated in every CTA's shared memory.
 constexpr int kSpecFr = 1024;     // frontier entries per CTA (shared memory)
 constexpr int kSpecCache = 64;    // results of evaluated, not yet popped nodes
-constexpr double kSpecWidth = 1.0 / 16;  // only intervals this narrow are speculated
+constexpr double kSpecWidth = 1.0;  // only intervals this narrow are speculated (all but the root)
 
 struct SpecSlot {
     double lo, hi, c, den_lo, den_c, den_hi;
@@ -1604,6 +1608,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
 {
     constexpr size_t kRegionA = SolveSmem<NT>::region_a;
+    constexpr int kPixCutThreads = pix_cut_threads<NT>();
     extern __shared__ __align__(16) unsigned char smem[];
     WarpQueue &wq = reinterpret_cast<WarpQueue *>(smem)[threadIdx.x >> 5];
     double *scratch = reinterpret_cast<double *>(smem);
