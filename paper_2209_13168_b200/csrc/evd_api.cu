@@ -823,10 +823,11 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     for (int w = 0; w < n_windows; w++) max_n = std::max(max_n, off[w + 1] - off[w]);
     // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
     // trace is on (k_solve has the probes)
-    // (2 slots measured best below ~0.5M events per window on the whole grid;
-    // the wide nodes of larger windows make speculation cost more than the
-    // rounds it saves, and small CTA groups have little fixed cost to save)
-    int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? 2 : 1;
+    // (on the whole grid: 3 slots measured best below 100 k events per window,
+    // 4 up to 0.5 M; the wide nodes of larger windows make speculation cost
+    // more than the rounds it saves, and small CTA groups have little fixed
+    // cost to save)
+    int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? (max_n < kSmallWindow ? 3 : 4) : 1;
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
     if (ctx->trace_on) spec_k = 1;
     // CTA size: small windows on the whole grid are latency-bound (384 fatter

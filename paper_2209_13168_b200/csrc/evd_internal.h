@@ -36,6 +36,11 @@ enum SolveMode : int { kModeRoot = 0, kModeNode = 1 };
 enum SolveStatus : int { kStatusOk = 0, kStatusIterLimit = 1, kStatusCapacity = 2 };
 
 // Device-resident BnB state (one per context); host reads it back at the end.
+#ifndef EVD_SPEC_KMAX
+#define EVD_SPEC_KMAX 4
+#endif
+constexpr int kSpecK = EVD_SPEC_KMAX;  // node evaluations per speculative round (k_solve_spec)
+
 struct SolveState {
     // node under evaluation
     double lo, hi, c, den_lo, den_c, den_hi;
@@ -50,12 +55,11 @@ struct SolveState {
     int status, pad;
     unsigned long long marks;  // pixel increments of all images over the solve
     // speculative rounds (k_solve_spec): per-slot accumulators by round parity
-    alignas(16) unsigned long long sacc[2][4][8];
+    alignas(16) unsigned long long sacc[2][kSpecK][8];
 };
 
 // Result of one window of evd_solve_windows / evd_solve.
 enum WindowStatus : int { kStatusEmpty = 3, kStatusSpecOverflow = 4 };
-constexpr int kSpecK = 4;  // node evaluations per speculative round (k_solve_spec)
 struct WindowResult {
     double nu, contrast, bound_gap;
     long long iterations, bound_evals, point_evals, max_fr;
