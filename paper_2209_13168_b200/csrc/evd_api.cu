@@ -796,7 +796,7 @@ namespace {
 // chunks; it now measures 1-3% slower at every size (cfg 1, 2, 3, 5), so it is
 // off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
 constexpr long long kFilterMinEvents = LLONG_MAX;
-constexpr long long kSpecMaxEvents = 500000;  // speculative rounds for windows below this
+constexpr long long kSpecMaxEvents = 2000000;  // speculative rounds for windows below this
 constexpr long long kSmallWindow = 100000;    // 384-thread CTAs below this (whole grid)
 constexpr long long kLargeWindow = 500000;    // 768-thread CTAs from this on (whole grid)
 
@@ -824,9 +824,9 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
     // trace is on (k_solve has the probes)
     // (on the whole grid: 3 slots measured best below 100 k events per window,
-    // 4 up to 0.5 M; the wide nodes of larger windows make speculation cost
-    // more than the rounds it saves, and small CTA groups have little fixed
-    // cost to save)
+    // 4 up to 2 M -- cfg 3 20.07 -> 19.86 ms; at cfg 5 (5.3 M) the wide nodes
+    // make speculation cost more than the rounds it saves, and small CTA
+    // groups have little fixed cost to save)
     int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? (max_n < kSmallWindow ? 3 : 4) : 1;
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
     if (ctx->trace_on) spec_k = 1;
