@@ -42,7 +42,7 @@ constexpr int pix_cut_threads() { return NT >= 768 ? 2 * EVD_PIX_CUT_THREADS : E
 #define EVD_BATCH_DIV 1
 #endif
 #ifndef EVD_GUIDED_WIDTH
-#define EVD_GUIDED_WIDTH (1.0 / 16)
+#define EVD_GUIDED_WIDTH (1.0 / 2)
 #endif
 constexpr double kGuidedWidth = EVD_GUIDED_WIDTH;  // nodes wider than this claim guided batches
 constexpr double kFilterWidth = 1.0 / 64;  // node widths that try the filtered path
