@@ -305,6 +305,9 @@ __global__ void __launch_bounds__(kThreads) k_bound_image(
 // Per-interval fully_inside / marks stay in registers; blocks are ordered
 // group-major so a group's 32 images stay in L2 while it is in flight.
 constexpr int kFrontGroup = 32;
+#ifndef EVD_FRONT_BPG
+#define EVD_FRONT_BPG 4  // event blocks per interval group, per SM
+#endif
 
 __global__ void __launch_bounds__(kThreads) k_frontier(
     const double *__restrict__ xc, const double *__restrict__ yc, const double *__restrict__ t,
@@ -2036,7 +2039,7 @@ void launch_frontier(const double *xc, const double *yc, const double *t, long l
     set_attrs();
     const int groups = (K + kFrontGroup - 1) / kFrontGroup;
     long long bpg = (n + kThreads - 1) / kThreads;
-    if (bpg > (long long)num_sms() * 4) bpg = (long long)num_sms() * 4;
+    if (bpg > (long long)num_sms() * EVD_FRONT_BPG) bpg = (long long)num_sms() * EVD_FRONT_BPG;
     if (bpg < 1) bpg = 1;
     static const bool exact_only = getenv("EVD_FRONTIER_FILTER") && getenv("EVD_FRONTIER_FILTER")[0] == '0';
     if (exact_only)
@@ -2071,7 +2074,7 @@ void launch_points_multi(const double *xc, const double *yc, const double *t, lo
 {
     const int groups = (K + 31) / 32;
     long long bpg = (n + kThreads - 1) / kThreads;
-    if (bpg > (long long)num_sms() * 4) bpg = (long long)num_sms() * 4;
+    if (bpg > (long long)num_sms() * EVD_FRONT_BPG) bpg = (long long)num_sms() * EVD_FRONT_BPG;
     if (bpg < 1) bpg = 1;
     k_points_multi<<<(unsigned)(groups * bpg), kThreads, 0, s>>>(xc, yc, t, n, nus, dens, K, cx,
                                                                  cy, W, H, images, M, (int)bpg,
