@@ -797,8 +797,12 @@ namespace {
 // off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
 constexpr long long kFilterMinEvents = LLONG_MAX;
 constexpr long long kSpecMaxEvents = 2000000;  // speculative rounds for windows below this
-constexpr long long kSmallWindow = 100000;    // 384-thread CTAs below this (whole grid)
-constexpr long long kLargeWindow = 500000;    // 768-thread CTAs from this on (whole grid)
+// CTA-size / slot-count policy for a whole-grid solve, from
+// tools/threshold_sweep.py (subsampled cfg 2 / cfg 3 windows and cfg 1):
+// 384 threads + 3 slots win at 20 k events, 512 + 4 slots at 50-150 k,
+// 512 and 768 tie at 204 k, 768 + 4 slots wins from 400 k
+constexpr long long kSmallWindow = 32768;     // 384-thread CTAs below this
+constexpr long long kLargeWindow = 250000;    // 768-thread CTAs from this on
 
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
@@ -823,8 +827,8 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     for (int w = 0; w < n_windows; w++) max_n = std::max(max_n, off[w + 1] - off[w]);
     // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
     // trace is on (k_solve has the probes)
-    // (on the whole grid: 3 slots measured best below 100 k events per window,
-    // 4 up to 2 M -- cfg 3 20.07 -> 19.86 ms; at cfg 5 (5.3 M) the wide nodes
+    // (on the whole grid: 3 slots measured best with 384-thread CTAs, 4 above,
+    // up to 2 M events -- cfg 3 20.07 -> 19.86 ms; at cfg 5 (5.3 M) the wide nodes
     // make speculation cost more than the rounds it saves, and small CTA
     // groups have little fixed cost to save)
     int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? (max_n < kSmallWindow ? 3 : 4) : 1;
