@@ -303,6 +303,35 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
     return d.chunks;
 }
 
+// Skipping the calls of plain crossings (cursor_step).  Take an X item P at
+// x ~ k (ddx > 0; ddx < 0 is the mirror image) whose y lies farther than
+// delta = 2^-30 (1 + |y|) from every integer.  Positions are monotone in s
+// and a crossing item lies within a few ulps (eps << delta) of its grid line,
+// so:
+//  * rows: a row line between P and the midpoint M1 before it (or M2 after
+//    it) would put that line's Y item strictly between the two samples
+//    around P, which are consecutive -- so M1, M2 and P share P's row, and
+//    M1, M2 are not on a row line;
+//  * columns: x is linear in s up to eps and the neighbouring samples lie in
+//    [k-1-eps, k+1+eps], so M1.x is in [k-1/2-eps, x_P] and M2.x in
+//    [x_P, k+1/2+eps].  P's closed squares are (floor(x_P), row), plus
+//    (k-1, row) when x_P == k exactly: x_P < k is M1's cell, x_P > k is M2's,
+//    and x_P == k gives M1 in column k-1 and M2 in column k (or a midpoint on
+//    the line, whose own call marks both).
+// So P's pixels are among those its neighbouring midpoints mark (their calls,
+// or an earlier call of the same event -- the dedup only drops repeats), and
+// skipping P's call leaves the pixel set, the image and the mark count
+// unchanged.  The leading / trailing samples and near-corner crossings take
+// the reference's closed-square call.
+#ifndef EVD_SKIP_PLAIN
+#define EVD_SKIP_PLAIN 1
+#endif
+__device__ __forceinline__ bool plain_crossing(double o)
+{
+    const double f = floor(o), slack = 0x1p-30 * (1.0 + fabs(o));
+    return o - f > slack && (f + 1.0) - o > slack;
+}
+
 // Resumable walk over one chunk's items: mark every item, then the midpoint
 // to its successor (contrast.py:176-182).  Each list keeps its next two item
 // values, so the division that refills a list is off the critical path.
@@ -314,6 +343,7 @@ struct Cursor {
     double sY, sY2;
     double kX, kY;        // grid coordinate of the item that enters each lookahead next
     double cur;           // item to mark next
+    int kind;             // origin of cur: 0 = the leading 0 / trailing 1, 1 = X list, 2 = Y list
     Prev prev;
 };
 
@@ -354,6 +384,7 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
         c.iX = 0;
         c.iY = 0;
         c.cur = 0.0;
+        c.kind = 0;
         c.prev = Prev{1, 0, 1, 0};
         c.sX = item_or_none(X, 0);
         c.sX2 = item_or_none(X, 1);
@@ -366,6 +397,7 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
         double first;
         if (p >= T) {
             first = 1.0;
+            c.kind = 0;
             c.fin = 1;
             c.iX = X.n;
             c.iY = Y.n;
@@ -374,6 +406,7 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
             const double xi = item_or_none(X, i), yj = item_or_none(Y, jy);
             if (xi <= yj) {  // X first on equal values
                 first = xi;
+                c.kind = 1;
                 c.iX = i + 1;
                 c.iY = jy;
                 c.sX = item_or_none(X, i + 1);
@@ -382,6 +415,7 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
                 c.sY2 = item_or_none(Y, jy + 1);
             } else {
                 first = yj;
+                c.kind = 2;
                 c.iX = i;
                 c.iY = jy + 1;
                 c.sX = xi;
@@ -416,8 +450,20 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
                                             int &marks)
 {
     const double cx0 = d.X.c0, ddx = d.X.dd, cy0 = d.Y.c0, ddy = d.Y.dd;
-    marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H, c.prev,
-                        sink);
+    // A grid-line crossing whose other coordinate is not near a grid line
+    // marks only pixels of the cells of the midpoints on either side of it,
+    // which mark them anyway (plain_crossing), so its call adds no pixel and
+    // is skipped; the leading / trailing samples and near-corner crossings
+    // take the reference's closed-square call.
+    if (EVD_SKIP_PLAIN && c.kind != 0) {
+        const double o = c.kind == 1 ? dadd(cy0, dmul(c.cur, ddy)) : dadd(cx0, dmul(c.cur, ddx));
+        if (!plain_crossing(o))
+            marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H,
+                                c.prev, sink);
+    } else {
+        marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H,
+                            c.prev, sink);
+    }
     if (c.fin) return false;  // the trailing ts = 1 has no successor
     const bool tX = c.sX < 2.0 && c.sX <= c.sY;
     const bool tY = !tX && c.sY < 2.0;
@@ -430,6 +476,7 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
         double v = ddiv(dsub(k, tX ? cx0 : cy0), tX ? ddx : ddy);
         v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
         if (idx >= lim) v = 2.0;
+        c.kind = tX ? 1 : 2;
         if (tX) {
             c.iX++;
             c.sX = c.sX2;
@@ -443,6 +490,7 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
         }
     } else {
         c.fin = 1;
+        c.kind = 0;
     }
     const double sm = dmul(0.5, dadd(c.cur, nxt));
     marks += mark_interior(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
