@@ -216,6 +216,35 @@ struct CrossList {
     }
 };
 
+// Skipping the calls of plain crossings (cursor_step).  Take an X item P at
+// x ~ k (ddx > 0; ddx < 0 is the mirror image) whose y lies farther than
+// delta = 2^-30 (1 + |y|) from every integer.  Positions are monotone in s
+// and a crossing item lies within a few ulps (eps << delta) of its grid line,
+// so:
+//  * rows: a row line between P and the midpoint M1 before it (or M2 after
+//    it) would put that line's Y item strictly between the two samples
+//    around P, which are consecutive -- so M1, M2 and P share P's row, and
+//    M1, M2 are not on a row line;
+//  * columns: x is linear in s up to eps and the neighbouring samples lie in
+//    [k-1-eps, k+1+eps], so M1.x is in [k-1/2-eps, x_P] and M2.x in
+//    [x_P, k+1/2+eps].  P's closed squares are (floor(x_P), row), plus
+//    (k-1, row) when x_P == k exactly: x_P < k is M1's cell, x_P > k is M2's,
+//    and x_P == k gives M1 in column k-1 and M2 in column k (or a midpoint on
+//    the line, whose own call marks both).
+// So P's pixels are among those its neighbouring midpoints mark (their calls,
+// or an earlier call of the same event -- the dedup only drops repeats), and
+// skipping P's call leaves the pixel set, the image and the mark count
+// unchanged.  The leading / trailing samples and near-corner crossings take
+// the reference's closed-square call.
+#ifndef EVD_SKIP_PLAIN
+#define EVD_SKIP_PLAIN 1
+#endif
+__device__ __forceinline__ bool plain_crossing(double o)
+{
+    const double f = floor(o), slack = 0x1p-30 * (1.0 + fabs(o));
+    return o - f > slack && (f + 1.0) - o > slack;
+}
+
 // A clipped segment ready for sampling.  Its sample sequence is
 // S = [0, merge(X, Y), 1] (np.sort of the reference's ts array: both lists are
 // monotone and clamped into [0, 1], so a two-way merge reproduces the sorted
@@ -283,17 +312,27 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
     // contrast.py:139-144
     d.X.init(dadd(ax, dmul(t0, dx)), dadd(ax, dmul(t1, dx)));
     d.Y.init(dadd(ay, dmul(t0, dy)), dadd(ay, dmul(t1, dy)));
-    if (d.X.n == 0 && d.Y.n == 0) {
-        // No crossings: the samples are ts = [0, 1] and the calls mark p(0),
-        // p(0.5), p(1).  If p(0) = (cx0, cy0) and p(1) = (cx0 + ddx, cy0 + ddy)
-        // lie strictly inside one pixel, so does p(0.5) (it lies between them
-        // coordinate-wise), and the three calls mark exactly that pixel.
+    {
+        // Short segments.  The samples p(s) = (cx0 + s ddx, cy0 + s ddy),
+        // s in [0, 1], are monotone in s, so every sample -- crossings and
+        // midpoints included -- lies in the box spanned by p(0) = (cx0, cy0)
+        // and p(1) = (cx0 + ddx, cy0 + ddy).  With both strictly inside their
+        // pixels and those pixels equal or edge-adjacent, every closed square
+        // containing a sample is one of the two, and the calls at p(0) and
+        // p(1) mark both: the segment marks exactly them (in the frame).
+        const double x0 = d.X.c0, y0 = d.Y.c0;
         const double x1 = dadd(d.X.c0, d.X.dd), y1 = dadd(d.Y.c0, d.Y.dd);
-        const double fx0 = floor(d.X.c0), fy0 = floor(d.Y.c0);
-        if (fx0 != d.X.c0 && fy0 != d.Y.c0 && floor(x1) == fx0 && floor(y1) == fy0 &&
-            x1 != fx0 && y1 != fy0) {
-            const long long p = floor_bin(d.X.c0, d.Y.c0, W, H);
-            if (p >= 0) { sink(p); marks++; }
+        const double fx0 = floor(x0), fy0 = floor(y0), fx1 = floor(x1), fy1 = floor(y1);
+        if (fx0 != x0 && fy0 != y0 && fx1 != x1 && fy1 != y1 &&
+            fabs(fx1 - fx0) + fabs(fy1 - fy0) <= 1.0) {
+            if (fx0 >= 0.0 && fx0 < W && fy0 >= 0.0 && fy0 < H) {
+                sink((long long)fy0 * W + (long long)fx0);
+                marks++;
+            }
+            if ((fx1 != fx0 || fy1 != fy0) && fx1 >= 0.0 && fx1 < W && fy1 >= 0.0 && fy1 < H) {
+                sink((long long)fy1 * W + (long long)fx1);
+                marks++;
+            }
             return 0;
         }
     }
@@ -301,35 +340,6 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
     d.chunks = (items + C - 1) / C;
     d.csize = C;
     return d.chunks;
-}
-
-// Skipping the calls of plain crossings (cursor_step).  Take an X item P at
-// x ~ k (ddx > 0; ddx < 0 is the mirror image) whose y lies farther than
-// delta = 2^-30 (1 + |y|) from every integer.  Positions are monotone in s
-// and a crossing item lies within a few ulps (eps << delta) of its grid line,
-// so:
-//  * rows: a row line between P and the midpoint M1 before it (or M2 after
-//    it) would put that line's Y item strictly between the two samples
-//    around P, which are consecutive -- so M1, M2 and P share P's row, and
-//    M1, M2 are not on a row line;
-//  * columns: x is linear in s up to eps and the neighbouring samples lie in
-//    [k-1-eps, k+1+eps], so M1.x is in [k-1/2-eps, x_P] and M2.x in
-//    [x_P, k+1/2+eps].  P's closed squares are (floor(x_P), row), plus
-//    (k-1, row) when x_P == k exactly: x_P < k is M1's cell, x_P > k is M2's,
-//    and x_P == k gives M1 in column k-1 and M2 in column k (or a midpoint on
-//    the line, whose own call marks both).
-// So P's pixels are among those its neighbouring midpoints mark (their calls,
-// or an earlier call of the same event -- the dedup only drops repeats), and
-// skipping P's call leaves the pixel set, the image and the mark count
-// unchanged.  The leading / trailing samples and near-corner crossings take
-// the reference's closed-square call.
-#ifndef EVD_SKIP_PLAIN
-#define EVD_SKIP_PLAIN 1
-#endif
-__device__ __forceinline__ bool plain_crossing(double o)
-{
-    const double f = floor(o), slack = 0x1p-30 * (1.0 + fabs(o));
-    return o - f > slack && (f + 1.0) - o > slack;
 }
 
 // Resumable walk over one chunk's items: mark every item, then the midpoint
