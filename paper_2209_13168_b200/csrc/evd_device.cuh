@@ -310,8 +310,8 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
         if (t0 > t1) return 0;
     }
     // contrast.py:139-144
-    d.X.init(dadd(ax, dmul(t0, dx)), dadd(ax, dmul(t1, dx)));
-    d.Y.init(dadd(ay, dmul(t0, dy)), dadd(ay, dmul(t1, dy)));
+    const double xs = dadd(ax, dmul(t0, dx)), xe = dadd(ax, dmul(t1, dx));
+    const double ys = dadd(ay, dmul(t0, dy)), ye = dadd(ay, dmul(t1, dy));
     {
         // Short segments.  The samples p(s) = (cx0 + s ddx, cy0 + s ddy),
         // s in [0, 1], are monotone in s, so every sample -- crossings and
@@ -320,8 +320,8 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
         // pixels and those pixels equal or edge-adjacent, every closed square
         // containing a sample is one of the two, and the calls at p(0) and
         // p(1) mark both: the segment marks exactly them (in the frame).
-        const double x0 = d.X.c0, y0 = d.Y.c0;
-        const double x1 = dadd(d.X.c0, d.X.dd), y1 = dadd(d.Y.c0, d.Y.dd);
+        const double x0 = xs, y0 = ys;
+        const double x1 = dadd(xs, dsub(xe, xs)), y1 = dadd(ys, dsub(ye, ys));
         const double fx0 = floor(x0), fy0 = floor(y0), fx1 = floor(x1), fy1 = floor(y1);
         if (fx0 != x0 && fy0 != y0 && fx1 != x1 && fy1 != y1 &&
             fabs(fx1 - fx0) + fabs(fy1 - fy0) <= 1.0) {
@@ -336,6 +336,8 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
             return 0;
         }
     }
+    d.X.init(xs, xe);
+    d.Y.init(ys, ye);
     const int items = 2 + d.X.n + d.Y.n;
     d.chunks = (items + C - 1) / C;
     d.csize = C;
