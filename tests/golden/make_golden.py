@@ -21,6 +21,8 @@ Fixtures:
   preproc.npz   pixel_counts / remove_hot_pixels / rescale_events (events.py:273-313)
                 outputs on test-suite streams, landing streams with injected hot
                 pixels, and rescale targets
+  nonfinite.npz / .json  point / bound images and BnB results for windows
+                with NaN, infinite and huge coordinates and NaN timestamps
   evd1.npz      EVD1 files (parse_event_bin, events.py:186-206): valid bodies
                 (sorted, unsorted with equal timestamps, large t_us) with the
                 reference's decoded arrays, and malformed / invalid bodies
@@ -439,6 +441,58 @@ def make_synth():
         json.dump(out, fh, indent=1)
 
 
+def make_nonfinite():
+    """Windows with NaN / infinite / huge coordinates and NaN timestamps (the
+    reference's EventBatch validates only the t range, so these reach the
+    path): point images, bound images and the BnB result."""
+    import warnings
+    rng = np.random.default_rng(4711)
+    out, meta = {}, []
+    w, h, n = 40, 30, 600
+    for case in range(4):
+        x = rng.uniform(0, w, n)
+        y = rng.uniform(0, h, n)
+        t = np.sort(rng.uniform(0, 0.5, n))
+        k = rng.choice(n, 40, replace=False)
+        if case == 0:
+            x[k[:20]] = np.nan
+            y[k[20:]] = np.nan
+        elif case == 1:
+            t[k] = np.nan
+        elif case == 2:
+            x[k[:20]] = np.inf
+            y[k[20:]] = -np.inf
+        else:
+            x[k[:20]] = 1e308
+            x[k[20:]] = -1e308
+        b = EventBatch(x, y, t, 0.5, SensorGeometry(w, h))
+        name = f"nf{case}"
+        out[f"{name}/x"], out[f"{name}/y"], out[f"{name}/t"] = x, y, t
+        lo0 = velocity_domain(0.5).lo
+        ivs = [(lo0, 0.0), (-0.5, -0.3), (-0.41, -0.4)]
+        rec = {"name": name, "width": w, "height": h, "points": [], "bounds": []}
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            for j, nu in enumerate([0.0, -0.4, lo0]):
+                img = con.accumulate_image(b, nu)
+                out[f"{name}/point{j}"] = img.counts.astype(np.uint32)
+                rec["points"].append({"nu": bits(nu), "in_image": img.in_image_events,
+                                      "contrast": bits(con.image_contrast(img))})
+            for j, (lo, hi) in enumerate(ivs):
+                ub = con.upper_bound_image(b, VelocityInterval(lo, hi))
+                bt = con.bound_terms(b, VelocityInterval(lo, hi))
+                out[f"{name}/bound{j}"] = ub.counts.astype(np.uint32)
+                rec["bounds"].append({"lo": bits(lo), "hi": bits(hi), "marks": ub.in_image_events,
+                                      "c_bar": bits(bt.c_bar)})
+            r = sol.maximise_contrast_bnb(b, sol.SolverParams())
+            rec["result"] = res_dict(r)
+        meta.append(rec)
+    np.savez_compressed(os.path.join(HERE, "nonfinite.npz"), **out)
+    with open(os.path.join(HERE, "nonfinite.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print("nonfinite:", len(meta), "cases")
+
+
 if __name__ == "__main__":
     big = "--big" in sys.argv
     what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["segments", "images", "bnb", "synth", "evd1", "preproc"]
@@ -454,3 +508,5 @@ if __name__ == "__main__":
         make_preproc()
     if "bnb" in what:
         make_bnb(big)
+    if "nonfinite" in what:
+        make_nonfinite()
