@@ -117,6 +117,36 @@ __device__ __forceinline__ bool sure_segment(const Warped &a, const Warped &b, d
     return true;
 }
 
+// sure_segment, also certifying edge-adjacent end cells: both exact end
+// samples surely strictly inside cells that are equal or share an edge mark
+// exactly those cells (build_segment's short-segment rule; the end sample
+// p(1) = a + (b - a) is within a few ulps of b, far inside the margin).
+// pix_b is -1 when the cells are equal.
+__device__ __forceinline__ bool sure_segment_adj(const Warped &a, const Warped &b, double ma,
+                                                 double mb, int W, int H, long long &pix_a,
+                                                 long long &pix_b, int &inside)
+{
+    const double sx = ma + mb + 1e-12 * (1.0 + fabs(a.x) + fabs(b.x));
+    const double sy = ma + mb + 1e-12 * (1.0 + fabs(a.y) + fabs(b.y));
+    pix_b = -1;
+    if ((a.x < -sx && b.x < -sx) || (a.x > W + sx && b.x > W + sx) ||
+        (a.y < -sy && b.y < -sy) || (a.y > H + sy && b.y > H + sy)) {
+        pix_a = -1;
+        inside = 0;
+        return true;
+    }
+    double fax, fay, fbx, fby;
+    if (!sure_cell(a.x, ma, fax) || !sure_cell(a.y, ma, fay) || !sure_cell(b.x, mb, fbx) ||
+        !sure_cell(b.y, mb, fby) || fabs(fax - fbx) + fabs(fay - fby) > 1.0)
+        return false;
+    const bool ia = fax >= 0.0 && fax < W && fay >= 0.0 && fay < H;
+    const bool ib = fbx >= 0.0 && fbx < W && fby >= 0.0 && fby < H;
+    inside = (ia && ib) ? 1 : 0;
+    pix_a = ia ? (long long)fay * W + (long long)fax : -1;
+    if (ib && (fax != fbx || fay != fby)) pix_b = (long long)fby * W + (long long)fbx;
+    return true;
+}
+
 // ---------------------------------------------------------------- supercover
 // Per-event dedup.  The reference marks each pixel at most once per event with
 // a stamp grid (contrast.py:89-91).  The device compares against the previous

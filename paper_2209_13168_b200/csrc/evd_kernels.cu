@@ -458,10 +458,11 @@ __global__ void __launch_bounds__(kThreads) k_frontier_f(
         }
         bool unc = false;
         if (valid) {
-            long long pix;
+            long long pix, pix2;
             int ins;
-            if (sure_segment(aq, bq, ma, mb, W, H, pix, ins)) {
+            if (sure_segment_adj(aq, bq, ma, mb, W, H, pix, pix2, ins)) {
                 if (pix >= 0) sink(pix);
+                if (pix2 >= 0) sink(pix2);
                 fi += ins;
             } else {
                 unc = true;
