@@ -23,6 +23,7 @@ Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -361,8 +362,10 @@ def run_gpu(args, rank, world, local):
                       "device_rounds": int(res.rounds)},
             "atomic_roofline": atomic,
             "limiter": limiter,
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n,
-                    "d2h_bytes_per_step": 272},  # SolveState read back (evd_internal.h)
+            # per step: x, y, t (f64) and the window offsets in; one WindowResult
+            # (evd_internal.h) out
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n + 16,
+                    "d2h_bytes_per_step": ctypes.sizeof(_lib.WindowResult)},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "roofline": {"bound": "hbm", "kernel": KERNEL, "achieved": achieved,
