@@ -75,3 +75,24 @@ def test_random_bound_images_like_the_oracle(seed):
             ref_counts, ref_fi = orc.bound_image(b, float(lo[j]), float(hi[j]))
             assert np.array_equal(ims[j], ref_counts), (seed, case, j)
             assert fi[j] == ref_fi and marks[j] == ref_counts.sum(dtype=np.uint64)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_frontiers_like_the_oracle(seed):
+    """The batched frontier (filtered first pass: off-frame / one-cell /
+    edge-adjacent certification, exact path for the rest) on adversarial
+    windows and uniform leaves of depth 3-9, against the oracle's integers."""
+    from paper_2209_13168_b200 import frontier as fr
+    r = np.random.default_rng(9090 + seed)
+    for case in range(10):
+        b = _window(r, case)
+        depth = int(r.integers(3, 10))
+        lo, hi = fr.uniform_frontier(velocity_domain(b.tau), depth)
+        pick = np.sort(r.choice(lo.size, min(lo.size, 40), replace=False))
+        lo, hi = lo[pick], hi[pick]
+        s_bar, fi, marks = con.frontier_terms(b, lo, hi)
+        for j in range(lo.size):
+            counts, ref_fi = orc.bound_image(b, float(lo[j]), float(hi[j]))
+            c64 = counts.astype(np.uint64)
+            assert (int(s_bar[j]), int(fi[j]), int(marks[j])) == (
+                int((c64 * c64).sum()), ref_fi, int(c64.sum())), (seed, case, j)
