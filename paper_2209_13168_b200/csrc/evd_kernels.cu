@@ -1917,6 +1917,11 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                     for (int s = 1; s < K; s++) {
                         const long long bi = spec_argmax(frs, Z.fr_n, [&](const FrontierEntry &e) {
                             if (dsub(e.hi, e.lo) > kSpecWidth) return true;
+                            // never evaluated by the reference: popping it ends
+                            // the search (solver.py:106-108; c_hat only grows)
+                            if (dsub(e.bound, Z.c_hat) <= a.gamma ||
+                                dsub(e.hi, e.lo) < a.min_width)
+                                return true;
                             for (int q = 0; q < Z.nslot; q++)
                                 if (Z.slot[q].counter == e.counter) return true;
                             return spec_find(Z, e.counter) >= 0;
