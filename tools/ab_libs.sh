@@ -1,3 +1,8 @@
+# Same-box A/B of two libevd builds: build_var/base.so (e.g. HEAD's sources
+# built with the Makefile's flags) and build_var/new.so (the working tree's
+# libevd.so copied there).  GPU tests on the working tree, then cfg 1-3 solve
+# times and the cfg-3 frontier for each library (EVD_LIB), twice, interleaved.
+# Outputs under gpurun_out/ab/.
 mkdir -p gpurun_out/ab
 python -m pytest tests -m gpu -q -x > gpurun_out/ab/gpu_tests.log 2>&1; tail -2 gpurun_out/ab/gpu_tests.log
 for r in 1 2; do for v in base new; do echo "== $v"; EVD_LIB=build_var/$v.so python tools/time_solve.py 1 2 3; done; done > gpurun_out/ab/time.log 2>&1
