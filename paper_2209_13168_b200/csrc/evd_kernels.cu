@@ -31,6 +31,14 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #define EVD_CHUNK 16
 #endif
 constexpr int kChunk = EVD_CHUNK;
+// The solve's 768-thread build (windows from 250 k events) samples in chunks
+// of 24: cfg 3 18.10 -> 17.96 ms, cfg 5 147.5 -> 144.3 ms; 16 stays best
+// below (cfg 1 0.947 vs 0.971 ms at 24, cfg 2 neutral).  Chunk size only
+// moves the seams, never the marks.
+#ifndef EVD_CHUNK_LARGE
+#define EVD_CHUNK_LARGE 24
+#endif
+constexpr int chunk_for(int nt) { return nt >= 768 ? EVD_CHUNK_LARGE : kChunk; }
 #ifndef EVD_PIX_CUT_THREADS
 #define EVD_PIX_CUT_THREADS 128
 #endif
@@ -91,12 +99,13 @@ struct WarpQueue {
 // Returns the number of queued chunks.  Every multi-pixel segment is queued:
 // a lane sampling its own short segment diverges from the others, and the
 // extra sampler copy costs registers and I-cache (measured slower).
+template <int C = kChunk>
 __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double bx, double by,
                                                     int W, int H, WarpQueue &q, int slot,
                                                     AtomicSink &sink, int &marks)
 {
     SegDesc d;
-    const int c = build_segment(ax, ay, bx, by, W, H, kChunk, d, sink, marks);
+    const int c = build_segment(ax, ay, bx, by, W, H, C, d, sink, marks);
     if (c == 0) return 0;
     q.d[slot] = d;
     q.img[slot] = sink.img;
@@ -107,20 +116,22 @@ __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double
 // child segments: one copy keeps the hot loop inside the instruction cache.
 // Plain-value interface (image pointer in, chunks | marks << 16 out): a
 // reference to the caller's sink or mark counter would live in local memory.
+template <int C = kChunk>
 __device__ __noinline__ int segment_or_queue_ool(double ax, double ay, double bx, double by,
                                                  int W, int H, WarpQueue &q, int slot,
                                                  unsigned int *img)
 {
     AtomicSink sink{img};
     int marks = 0;
-    const int c = segment_or_queue_inl(ax, ay, bx, by, W, H, q, slot, sink, marks);
+    const int c = segment_or_queue_inl<C>(ax, ay, bx, by, W, H, q, slot, sink, marks);
     return c | (marks << 16);  // chunks < 2^16 (W + H + 4 items / kChunk)
 }
+template <int C = kChunk>
 __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,
                                                 int H, WarpQueue &q, int slot,
                                                 const AtomicSink &sink, int &marks)
 {
-    const int r = segment_or_queue_ool(ax, ay, bx, by, W, H, q, slot, sink.img);
+    const int r = segment_or_queue_ool<C>(ax, ay, bx, by, W, H, q, slot, sink.img);
     marks += r >> 16;
     return r & 0xffff;
 }
@@ -829,6 +840,7 @@ struct EventJob {
     int guided;  // shrink claims as the counter runs out (wide nodes)
 };
 
+template <int C = kChunk>
 __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &wq,
                                                  unsigned long long (&v)[4],
                                                  unsigned long long (&vex)[1])
@@ -870,12 +882,12 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
             }
             if (j.mode == kModeRoot) {
                 v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
-                cA = segment_or_queue(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
+                cA = segment_or_queue<C>(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
             } else {
                 v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
-                cA = segment_or_queue(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
+                cA = segment_or_queue<C>(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
                 v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
-                cB = segment_or_queue(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb, dummy);
+                cB = segment_or_queue<C>(wc.x, wc.y, wh.x, wh.y, W, H, wq, 2 * lane + 1, sb, dummy);
             }
             vex[0]++;
         }
@@ -1318,7 +1330,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
             if (!FILTER || dsub(hi, lo) > kFilterWidth) {
                 EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
                            W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth};
-                event_pass_exact(J, wq, v, vex);
+                event_pass_exact<chunk_for(NT)>(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
                 long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
@@ -1688,7 +1700,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 EventJob J{xc, yc, tw, n, sl.lo, sl.c, sl.hi, sl.den_lo, sl.den_c, sl.den_hi,
                            a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
                            gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth};
-                event_pass_exact(J, wq, v, vex);
+                event_pass_exact<chunk_for(NT)>(J, wq, v, vex);
 #pragma unroll
                 for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);
                 vex[0] = warp_sum(vex[0]);
