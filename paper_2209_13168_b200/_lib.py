@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 
 import numpy as np
@@ -121,6 +122,7 @@ _lib = None
 _lib_lock = threading.Lock()
 _tls = threading.local()
 _default_device = int(os.environ.get("EVD_DEVICE", "0"))
+_explicit_device: int | None = None
 
 
 def load():
@@ -143,8 +145,8 @@ def load():
 
 def set_device(device: int) -> None:
     """Device used by contexts created afterwards in this process."""
-    global _default_device
-    _default_device = int(device)
+    global _explicit_device
+    _explicit_device = int(device)
 
 
 class Context:
@@ -183,9 +185,26 @@ class Context:
         return int(self.lib.evd_device_sms(self.h))
 
 
+def _current_device() -> int:
+    """set_device's choice; else torch's current device once torch has
+    initialised CUDA in this process (one rank per GPU under torch.distributed
+    calls torch.cuda.set_device(local_rank)); else EVD_DEVICE / 0."""
+    if _explicit_device is not None:
+        return _explicit_device
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    return _default_device
+
+
 def context(device: int | None = None) -> Context:
-    """The calling thread's context for `device` (default: set_device / EVD_DEVICE / 0)."""
-    dev = _default_device if device is None else int(device)
+    """The calling thread's context for `device` (default: set_device, else
+    torch's current CUDA device, else EVD_DEVICE / 0)."""
+    dev = _current_device() if device is None else int(device)
     cache = getattr(_tls, "ctx", None)
     if cache is None:
         cache = _tls.ctx = {}

@@ -68,9 +68,22 @@ def load_window(batch: EventBatch, ctx=None):
 
 def load_window_device(x, y, t, tau: float, geometry, ctx=None):
     """evd_set_events from device arrays on the context's GPU (torch CUDA
-    tensors of float64, contiguous), e.g. a window broadcast over NCCL."""
+    tensors of float64, contiguous), e.g. a window broadcast over NCCL.
+
+    The context is the tensors' own device's.  libevd copies on its own
+    stream, so the producer's stream (torch's current stream: the NCCL
+    broadcast that filled the tensors is ordered before it) is synchronised
+    first -- otherwise the copy could read the buffer before it is filled."""
     import ctypes
-    ctx = ctx or _lib.context()
+
+    import torch
+    dev = t.device.index if t.is_cuda else None
+    if ctx is None:
+        ctx = _lib.context(dev)
+    elif dev is not None and ctx.device != dev:
+        raise ValueError(f"events on cuda:{dev} but the libevd context is on cuda:{ctx.device}")
+    if t.is_cuda:
+        torch.cuda.current_stream(t.device).synchronize()
     n = int(t.numel())
     ptr = lambda v: ctypes.cast(ctypes.c_void_p(v.data_ptr()), _lib._d)
     rc = ctx.lib.evd_set_events(ctx.h, ptr(x), ptr(y), ptr(t), n, geometry.width,

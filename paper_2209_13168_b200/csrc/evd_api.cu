@@ -385,6 +385,17 @@ int check_den(evd_ctx *ctx, double nu, double tau, double *den)
     return EVD_OK;
 }
 
+// Frame sizes the kernels support: pixel ids fit int (W*H < 2^31) and a
+// segment's sample chunks fit the 16-bit field of segment_or_queue_ool's
+// packed return (chunks <= (W + H + 4) / C with C >= 1).
+int check_frame(evd_ctx *ctx, long long W, long long H)
+{
+    if (W + H + 4 >= 65536 || W * H >= (1ll << 31))
+        return fail(ctx, EVD_ERR_ARG, "sensor %lldx%lld exceeds the supported frame (W+H < 65532, W*H < 2^31)",
+                    W, H);
+    return EVD_OK;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -493,6 +504,7 @@ int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double 
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (n < 0 || width < 1 || height < 1)
         return fail(ctx, EVD_ERR_ARG, "bad window: n=%lld %dx%d", (long long)n, width, height);
+    if (int rc = check_frame(ctx, width, height)) return rc;
     if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "batch duration tau must be positive");
     if (n > 0 && (!x || !y || !t)) return fail(ctx, EVD_ERR_ARG, "NULL event array");
     CU(cudaSetDevice(ctx->device));
@@ -507,6 +519,9 @@ int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double 
         launch_center(ctx->xc.p, ctx->yc.p, n, width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p,
                       ctx->stream);
         LAUNCHED(1);
+        // inputs are never retained (evd.h): the caller may reuse or free
+        // x, y, t (pinned host or device memory) once this call returns
+        CU(cudaStreamSynchronize(ctx->stream));
     }
     ctx->n = n;
     ctx->W = width;
@@ -769,6 +784,7 @@ int evd_rasterize_segments(evd_ctx *ctx, const double *segs, int32_t k, int32_t 
 {
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (width < 1 || height < 1 || k < 0) return fail(ctx, EVD_ERR_ARG, "bad raster request");
+    if (int rc = check_frame(ctx, width, height)) return rc;
     if (k == 0) return EVD_OK;
     const size_t M = (size_t)width * height;
     CU(cudaSetDevice(ctx->device));
@@ -1047,6 +1063,7 @@ static int solve_resident_stream(evd_ctx *ctx, double tau, int groups,
     if (device_ms) *device_ms = 0.0;
     const long long n = ctx->sn;
     if (n == 0) return EVD_OK;  // batch_stream of an empty stream: no windows
+    if (int rc = check_frame(ctx, ctx->sW, ctx->sH)) return rc;
     double tt[2];
     CU(cudaMemcpyAsync(tt, ctx->st.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(tt + 1, ctx->st.p + n - 1, sizeof(double), cudaMemcpyDeviceToHost,
@@ -1107,6 +1124,7 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (!params || !n_windows || !k0_out || n < 0 || width < 1 || height < 1)
         return fail(ctx, EVD_ERR_ARG, "bad evd_solve_stream arguments");
+    if (int rc = check_frame(ctx, width, height)) return rc;
     if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "tau must be positive");
     if (n > 0 && (!x || !y || !t)) return fail(ctx, EVD_ERR_ARG, "NULL event array");
     CU(cudaSetDevice(ctx->device));
@@ -1212,6 +1230,7 @@ int evd_load_stream(evd_ctx *ctx, const double *x, const double *y, const double
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (n < 0 || width < 1 || height < 1 || (n > 0 && (!x || !y || !t)))
         return fail(ctx, EVD_ERR_ARG, "bad evd_load_stream arguments");
+    if (int rc = check_frame(ctx, width, height)) return rc;
     CU(cudaSetDevice(ctx->device));
     const long long m = std::max<long long>(n, 1);
     CU(ctx->sx.ensure(m));
@@ -1222,7 +1241,8 @@ int evd_load_stream(evd_ctx *ctx, const double *x, const double *y, const double
         CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
         CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
         CU(cudaMemcpyAsync(ctx->st.p, t, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
-        if (p) CU(cudaMemcpyAsync(ctx->sp.p, p, n, cudaMemcpyHostToDevice, ctx->stream));
+        if (p) CU(cudaMemcpyAsync(ctx->sp.p, p, n, cudaMemcpyDefault, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));  // inputs are never retained (evd.h)
     }
     ctx->sn = n;
     ctx->sW = width;

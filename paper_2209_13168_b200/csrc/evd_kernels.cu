@@ -124,7 +124,7 @@ __device__ __noinline__ int segment_or_queue_ool(double ax, double ay, double bx
     AtomicSink sink{img};
     int marks = 0;
     const int c = segment_or_queue_inl<C>(ax, ay, bx, by, W, H, q, slot, sink, marks);
-    return c | (marks << 16);  // chunks < 2^16 (W + H + 4 items / kChunk)
+    return c | (marks << 16);  // chunks <= (W + H + 4) / C < 2^16 (check_frame), marks <= 2
 }
 template <int C = kChunk>
 __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx, double by, int W,

@@ -214,7 +214,10 @@ def solve_batched(batch, params, k: int = 64, contrasts: Callable | None = None,
             gap_out = max(gap, 0.0)
             break
         batch_nodes = []
-        while heap and len(batch_nodes) < k:
+        # never expand past the cap: the reference raises right after the node
+        # that reaches it (solver.py:118-119)
+        room = min(k, params.max_iterations - nodes)
+        while heap and len(batch_nodes) < room:
             neg, _, lo, hi = heap[0]
             if -neg - c_hat <= params.gamma or hi - lo < params.min_interval_width:
                 break
@@ -234,6 +237,9 @@ def solve_batched(batch, params, k: int = 64, contrasts: Callable | None = None,
         for lo, hi, b in zip(clo, chi, cb):
             if b >= c_hat:  # solver.py:116
                 heapq.heappush(heap, (-float(b), next(ctr), float(lo), float(hi)))
+        if nodes >= params.max_iterations:  # solver.py:118-119, incumbent carried
+            from .solver import IterationLimitError
+            raise IterationLimitError(nu_hat, c_hat, nodes)
     return BatchedResult(nu_hat, c_hat, gap_out, rounds, nodes, evals)
 
 

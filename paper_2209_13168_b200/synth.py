@@ -5,7 +5,7 @@ reference simulator's trajectory model (``pkg/src/eventdiv/simulator.py:74-145``
 with the per-scene-point Python loop vectorised; every floating-point
 operation is the same elementwise IEEE operation in the same order, so the
 generated streams are bit-identical to ``generate_landing_events`` for the
-noise-free configurations used here (checked by ``tests/test_synth.py`` against
+noise-free configurations used here (checked by ``tests/test_host.py`` against
 fixtures produced by the reference itself).
 
 Configurations follow SURVEY.md §8(d).

@@ -17,7 +17,7 @@ from conftest import GOLDEN, ROOT, f64
 from oracle import oracle as orc
 from paper_2209_13168_b200 import dist as pdist
 from paper_2209_13168_b200.geometry import DivergenceSample, divergence_from_velocity
-from paper_2209_13168_b200.solver import SolverParams
+from paper_2209_13168_b200.solver import IterationLimitError, SolverParams
 
 
 def _free_port():
@@ -63,12 +63,19 @@ def _worker(rank, world, port, queue):
         b = wins[1]
         c, bd = _oracle_evaluators(b)
         res = pdist.solve_batched(b, params, k=8, contrasts=c, bounds=bd, split=True)
+        # the iteration cap holds in the split solve too, incumbent carried
+        try:
+            pdist.solve_batched(b, SolverParams(max_iterations=3), k=2, contrasts=c, bounds=bd,
+                                split=True)
+            capped = None
+        except IterationLimitError as e:
+            capped = (e.nu, e.contrast, e.iterations)
         # the window's events from rank 0 to every rank (one packed broadcast)
         x, y, t, tau, geom = pdist.broadcast_window(b if rank == 0 else None)
         same = (np.array_equal(x.numpy(), b.x) and np.array_equal(y.numpy(), b.y) and
                 np.array_equal(t.numpy(), b.t) and tau == b.tau and geom == b.geometry)
         queue.put((rank, [(s.t, s.contrast, s.iterations) for s in samples],
-                   (res.nu, res.contrast, res.rounds, res.nodes), same))
+                   (res.nu, res.contrast, res.rounds, res.nodes), same, capped))
     finally:
         dist.destroy_process_group()
 
@@ -95,9 +102,11 @@ def test_world2_gloo_windows_and_split_frontier():
         p.join(timeout=60)
         assert p.exitcode == 0
     outs.sort(key=lambda o: o[0])
-    (_, s0, r0, b0), (_, s1, r1, b1) = outs
+    (_, s0, r0, b0, c0), (_, s1, r1, b1, c1) = outs
     # both ranks hold the full, identical sample list and the identical BnB state
     assert s0 == s1 and r0 == r1
+    # both ranks stop at the cap with the same incumbent
+    assert c0 is not None and c0 == c1 and c0[2] == 3
     assert b0 and b1  # the broadcast window equals the source batch on both ranks
     serial = _oracle_stream(_windows(), SolverParams())
     assert s0 == [(s.t, s.contrast, s.iterations) for s in serial]
@@ -120,3 +129,17 @@ def test_batched_matches_reference_within_gamma_on_goldens(bnb_golden):
         ref_c = f64(w["result"]["contrast"])
         assert res.contrast >= ref_c - 0.025
         assert res.bound_gap <= 0.025 + 1e-12
+
+
+def test_batched_iteration_cap_carries_incumbent():
+    """solve_batched stops at params.max_iterations like solver.py:118-119:
+    IterationLimitError carrying the incumbent after exactly that many nodes."""
+    b = _windows()[1]
+    c, bd = _oracle_evaluators(b)
+    full = pdist.solve_batched(b, SolverParams(), k=4, contrasts=c, bounds=bd)
+    assert full.nodes > 5
+    for cap in (1, 5):
+        with pytest.raises(IterationLimitError) as ei:
+            pdist.solve_batched(b, SolverParams(max_iterations=cap), k=4, contrasts=c, bounds=bd)
+        assert ei.value.iterations == cap
+        assert ei.value.contrast <= full.contrast
