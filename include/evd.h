@@ -90,11 +90,39 @@ int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k
                      uint32_t *counts);
 
 /* Batched frontier: bound_terms (contrast.py:241-251) for k intervals in one
- * pass over the resident window (events held in registers across groups of
- * consecutive intervals; adjacent intervals sharing an endpoint share its
- * warp).  Same outputs as evd_bound_images without images. */
+ * call over the resident window.  Same outputs as evd_bound_images without
+ * images.  Paths (evd_set_option "frontier_path"):
+ *  EVD_FRONTIER_TILES        the window is binned once into angular tiles
+ *                            about the FOE (nu-invariant: the radial warp keeps
+ *                            each event on its ray); each CTA evaluates a
+ *                            (tile, 32 intervals) item with the 32 tile images
+ *                            in shared memory and reduces them on chip -- no
+ *                            image ever reaches HBM.  Needs every hi <= 0 and
+ *                            finite events (the reference domain is [lo0, 0]);
+ *  EVD_FRONTIER_GLOBAL       K x M u32 images in HBM (at most
+ *                            "frontier_image_budget" bytes per launch, larger
+ *                            k in chunks), filtered warp + exact fallback;
+ *  EVD_FRONTIER_GLOBAL_EXACT the same with exact warps only;
+ *  EVD_FRONTIER_AUTO         tiles when they apply, else global (default).
+ * Every path returns identical integers. */
+enum {
+    EVD_FRONTIER_AUTO = 0,
+    EVD_FRONTIER_TILES = 1,
+    EVD_FRONTIER_GLOBAL = 2,
+    EVD_FRONTIER_GLOBAL_EXACT = 3
+};
 int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
                       uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks);
+
+/* Per-context options: "frontier_path" (EVD_FRONTIER_*), "frontier_image_budget"
+ * (bytes of HBM images per global-path launch, default 8 GiB). */
+int evd_set_option(evd_ctx *ctx, const char *name, int64_t value);
+
+/* Diagnostics of the tiled frontier: out[0] tiles of the frame (0: not
+ * tiled), out[1] largest tile (pixels), out[2] events listed over all tiles
+ * for the resident window (-1: not binned or not usable), out[3] tiles with
+ * work, out[4] path of the last evd_eval_frontier call (EVD_FRONTIER_*). */
+int evd_frontier_info(evd_ctx *ctx, int64_t *out);
 
 /* image_contrast (contrast.py:61-64) of a caller image: np.sum((c - mean)**2)/M
  * with numpy's pairwise summation order; mean = in_image / m. */

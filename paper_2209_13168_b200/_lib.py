@@ -20,12 +20,14 @@ LIB_PATH = os.environ.get("EVD_LIB") or os.path.join(HERE, "libevd.so")
 EVD_OK, EVD_ERR_CUDA, EVD_ERR_ARG, EVD_ERR_NO_EVENTS = 0, 1, 2, 3
 EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
 EVD_ERR_FORMAT, EVD_ERR_VALIDATION = 7, 8
+FRONTIER_AUTO, FRONTIER_TILES, FRONTIER_GLOBAL, FRONTIER_GLOBAL_EXACT = 0, 1, 2, 3
 
 # every symbol include/evd.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
     "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
     "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
-    "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_image_contrast",
+    "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_set_option",
+    "evd_frontier_info", "evd_image_contrast",
     "evd_rasterize_segments",
     "evd_solve", "evd_solve_windows", "evd_solve_trace", "evd_solve_block_trace",
     "evd_probe_events", "evd_solve_stream", "evd_solve_loaded_stream", "evd_load_bin",
@@ -93,6 +95,8 @@ _SIGS = {
     "evd_point_images": (ctypes.c_int, [_vp, _d, _i32, _i64p, _d, _u32p]),
     "evd_bound_images": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p, _u32p]),
     "evd_eval_frontier": (ctypes.c_int, [_vp, _d, _d, _i32, _u64p, _i64p, _u64p]),
+    "evd_set_option": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64]),
+    "evd_frontier_info": (ctypes.c_int, [_vp, _i64p]),
     "evd_image_contrast": (ctypes.c_int, [_vp, _d, _i64, _i64, _d]),
     "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _i32, _u32p]),
     "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
@@ -183,6 +187,19 @@ class Context:
     @property
     def sms(self) -> int:
         return int(self.lib.evd_device_sms(self.h))
+
+    def set_option(self, name: str, value: int) -> None:
+        rc = self.lib.evd_set_option(self.h, name.encode(), int(value))
+        if rc:
+            raise EvdError(rc, self.error_text())
+
+    def frontier_info(self) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        rc = self.lib.evd_frontier_info(self.h, out.ctypes.data_as(_i64p))
+        if rc:
+            raise EvdError(rc, self.error_text())
+        return {"tiles": int(out[0]), "tile_pixels": int(out[1]), "listed_events": int(out[2]),
+                "tiles_with_work": int(out[3]), "last_path": int(out[4])}
 
 
 def _current_device() -> int:

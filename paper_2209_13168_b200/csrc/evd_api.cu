@@ -111,6 +111,13 @@ struct evd_ctx {
     bool trace_on = false;  // EVD_TRACE=1 at evd_create: record solve timelines
     int solve_blocks = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // resident-window generation (bumped whenever xc / yc / t change)
+    unsigned long long gen = 0;
+    // batched frontier (evd_eval_frontier)
+    FrontierTiles *tiles = nullptr;
+    int frontier_path = EVD_FRONTIER_AUTO;    // evd_set_option("frontier_path")
+    long long frontier_budget = 8ll << 30;    // image bytes of the global-image paths
+    int last_frontier_path = -1;
 };
 
 namespace {
@@ -476,6 +483,7 @@ void evd_destroy(evd_ctx *ctx)
     tp.trip.release();
     tp.top.release();
     tp.cutval.release();
+    tiles_free(ctx->tiles);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -524,6 +532,7 @@ int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double 
         CU(cudaStreamSynchronize(ctx->stream));
     }
     ctx->n = n;
+    ctx->gen++;
     ctx->W = width;
     ctx->H = height;
     ctx->tau = tau;
@@ -717,23 +726,16 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
     if (k == 0) return EVD_OK;
     const long long M = (long long)ctx->W * ctx->H;
     std::vector<double> host(4 * (size_t)k);
+    bool nonpositive = true;  // every nu <= 0: the warp scale is >= 1 (tiled path)
     for (int j = 0; j < k; j++) {
         if (lo[j] > hi[j]) return fail(ctx, EVD_ERR_ARG, "empty interval [%.17g, %.17g]", lo[j], hi[j]);
         if ((rc = check_den(ctx, lo[j], ctx->tau, &host[2 * (size_t)k + j]))) return rc;
         if ((rc = check_den(ctx, hi[j], ctx->tau, &host[3 * (size_t)k + j]))) return rc;
         host[j] = lo[j];
         host[(size_t)k + j] = hi[j];
+        nonpositive = nonpositive && hi[j] <= 0.0;
     }
     CU(cudaSetDevice(ctx->device));
-    // images of up to kb intervals at a time (kept zeroed between calls)
-    const long long cap_bytes = 8ll << 30;
-    long long kb = std::max<long long>(1, cap_bytes / (M * 4));
-    kb = std::min<long long>(kb, k);
-    kb = (kb + kFrontGroupHost - 1) / kFrontGroupHost * kFrontGroupHost;
-    if ((long long)ctx->fimg.cap < kb * M) {
-        CU(ctx->fimg.ensure((size_t)(kb * M)));
-        CU(cudaMemsetAsync(ctx->fimg.p, 0, ctx->fimg.cap * sizeof(unsigned int), ctx->stream));
-    }
     CU(ctx->fargs.ensure(4 * (size_t)k));
     CU(ctx->facc.ensure(3 * (size_t)k));
     CU(cudaMemcpyAsync(ctx->fargs.p, host.data(), host.size() * sizeof(double),
@@ -741,12 +743,42 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
     CU(cudaMemsetAsync(ctx->facc.p, 0, 3 * (size_t)k * sizeof(unsigned long long), ctx->stream));
     const double *d_lo = ctx->fargs.p, *d_hi = d_lo + k, *d_dl = d_lo + 2 * k, *d_dh = d_lo + 3 * k;
     unsigned long long *f_fi = ctx->facc.p, *f_ms = f_fi + k;  // fi[k], then (marks, s_bar)[k]
-    for (long long j0 = 0; j0 < k; j0 += kb) {
-        const int kk = (int)std::min<long long>(kb, k - j0);
-        launch_frontier(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, d_lo + j0, d_hi + j0, d_dl + j0,
-                        d_dh + j0, kk, ctx->W / 2.0, ctx->H / 2.0, ctx->W, ctx->H, ctx->fimg.p, M,
-                        f_fi + j0, f_ms + 2 * j0, ctx->stream);
-        LAUNCHED(2);
+    const int path = ctx->frontier_path;
+    bool tiled = false;
+    if ((path == EVD_FRONTIER_AUTO || path == EVD_FRONTIER_TILES) && nonpositive && ctx->n > 0) {
+        if (!ctx->tiles) ctx->tiles = tiles_new();
+        int nl = 0;
+        CU(tiles_bin(ctx->tiles, ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, ctx->W, ctx->H, ctx->gen,
+                     &tiled, &nl, ctx->stream));
+        LAUNCHED(nl);
+    }
+    if (path == EVD_FRONTIER_TILES && !tiled && ctx->n > 0)
+        return fail(ctx, EVD_ERR_STATE, "tiled frontier does not apply to this window/intervals "
+                                        "(frame not tileable, non-finite events, nu > 0 or a "
+                                        "tile over 65535 events)");
+    if (tiled) {
+        int nl = 0;
+        CU(tiles_eval(ctx->tiles, d_lo, d_hi, d_dl, d_dh, k, f_fi, f_ms, &nl, ctx->stream));
+        LAUNCHED(nl);
+        ctx->last_frontier_path = EVD_FRONTIER_TILES;
+    } else if (ctx->n > 0) {
+        // images of up to kb intervals at a time in HBM (kept zeroed between calls)
+        const bool exact_only = path == EVD_FRONTIER_GLOBAL_EXACT;
+        long long kb = std::max<long long>(1, ctx->frontier_budget / (M * 4));
+        kb = std::min<long long>(kb, k);
+        kb = (kb + kFrontGroupHost - 1) / kFrontGroupHost * kFrontGroupHost;
+        if ((long long)ctx->fimg.cap < kb * M) {
+            CU(ctx->fimg.ensure((size_t)(kb * M)));
+            CU(cudaMemsetAsync(ctx->fimg.p, 0, ctx->fimg.cap * sizeof(unsigned int), ctx->stream));
+        }
+        for (long long j0 = 0; j0 < k; j0 += kb) {
+            const int kk = (int)std::min<long long>(kb, k - j0);
+            launch_frontier(ctx->xc.p, ctx->yc.p, ctx->t.p, ctx->n, d_lo + j0, d_hi + j0, d_dl + j0,
+                            d_dh + j0, kk, ctx->W / 2.0, ctx->H / 2.0, ctx->W, ctx->H, ctx->fimg.p, M,
+                            f_fi + j0, f_ms + 2 * j0, exact_only, ctx->stream);
+            LAUNCHED(2);
+        }
+        ctx->last_frontier_path = exact_only ? EVD_FRONTIER_GLOBAL_EXACT : EVD_FRONTIER_GLOBAL;
     }
     std::vector<unsigned long long> out(3 * (size_t)k);
     CU(cudaMemcpyAsync(out.data(), ctx->facc.p, out.size() * sizeof(unsigned long long),
@@ -757,6 +789,34 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
         if (marks) marks[j] = out[(size_t)k + 2 * j];
         if (s_bar) s_bar[j] = out[(size_t)k + 2 * j + 1];
     }
+    return EVD_OK;
+}
+
+int evd_set_option(evd_ctx *ctx, const char *name, int64_t value)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (!name) return fail(ctx, EVD_ERR_ARG, "option name is NULL");
+    if (!strcmp(name, "frontier_path")) {
+        if (value < EVD_FRONTIER_AUTO || value > EVD_FRONTIER_GLOBAL_EXACT)
+            return fail(ctx, EVD_ERR_ARG, "frontier_path %lld out of range", (long long)value);
+        ctx->frontier_path = (int)value;
+        return EVD_OK;
+    }
+    if (!strcmp(name, "frontier_image_budget")) {
+        if (value < 1) return fail(ctx, EVD_ERR_ARG, "frontier_image_budget must be positive");
+        ctx->frontier_budget = value;
+        return EVD_OK;
+    }
+    return fail(ctx, EVD_ERR_ARG, "unknown option '%s'", name);
+}
+
+int evd_frontier_info(evd_ctx *ctx, int64_t *out)
+{
+    if (!ctx || !out) return fail(ctx, EVD_ERR_ARG, "NULL argument");
+    long long v[4] = {0, 0, -1, 0};
+    if (ctx->tiles) tiles_info(ctx->tiles, v);
+    for (int i = 0; i < 4; i++) out[i] = v[i];
+    out[4] = ctx->last_frontier_path;
     return EVD_OK;
 }
 
@@ -1103,6 +1163,7 @@ static int solve_resident_stream(evd_ctx *ctx, double tau, int groups,
         LAUNCHED(1);
     }
     ctx->n = total;
+    ctx->gen++;
     ctx->W = ctx->sW;
     ctx->H = ctx->sH;
     ctx->tau = tau;

@@ -160,6 +160,9 @@ struct Prev {
     int x0, x1, y0, y1;  // previous call's closed-square pixel range (inclusive)
 };
 
+// Sinks take a pixel as (row-major index p, column, row); sinks that index a
+// full image use p, the tiled frontier (evd_frontier_tiles.cu) uses (x, y).
+//
 // Pixel range [x0, x1] x [y0, y1] of the closed unit squares containing (px, py)
 // (contrast.py:73-91).  Points reaching here come from a segment clipped to
 // the frame, so the ranges fit in int.
@@ -184,10 +187,10 @@ __device__ __forceinline__ int mark_point(double px, double py, int W, int H, Pr
     const bool fy0 = (unsigned)r.y0 < (unsigned)H, fy1 = sy && (unsigned)r.y1 < (unsigned)H;
     const int base = r.y0 * W + r.x0;  // the frame has < 2^31 pixels
     int marks = 0;
-    if (fx0 && fy0 && !(px0 && py0)) { sink(base); marks++; }
-    if (fx1 && fy0 && !(px1 && py0)) { sink(base + 1); marks++; }
-    if (fx0 && fy1 && !(px0 && py1)) { sink(base + W); marks++; }
-    if (fx1 && fy1 && !(px1 && py1)) { sink(base + W + 1); marks++; }
+    if (fx0 && fy0 && !(px0 && py0)) { sink(base, r.x0, r.y0); marks++; }
+    if (fx1 && fy0 && !(px1 && py0)) { sink(base + 1, r.x1, r.y0); marks++; }
+    if (fx0 && fy1 && !(px0 && py1)) { sink(base + W, r.x0, r.y1); marks++; }
+    if (fx1 && fy1 && !(px1 && py1)) { sink(base + W + 1, r.x1, r.y1); marks++; }
     prev = r;
     return marks;
 }
@@ -205,7 +208,7 @@ __device__ __forceinline__ int mark_interior(double px, double py, int W, int H,
         const bool seen = ix >= prev.x0 && ix <= prev.x1 && iy >= prev.y0 && iy <= prev.y1;
         prev = Prev{ix, ix, iy, iy};
         if (!seen && (unsigned)ix < (unsigned)W && (unsigned)iy < (unsigned)H) {
-            sink(iy * W + ix);
+            sink(iy * W + ix, ix, iy);
             return 1;
         }
         return 0;
@@ -299,7 +302,7 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
 {
     if (ax == bx && ay == by) {  // degenerate: floor rule, not the closed-square rule
         const long long p = floor_bin(ax, ay, W, H);
-        if (p >= 0) { sink(p); marks++; }
+        if (p >= 0) { sink(p, (int)(p % W), (int)(p / W)); marks++; }
         return 0;
     }
     // Division-free rejection, exact: every sample the reference would mark
@@ -356,11 +359,11 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
         if (fx0 != x0 && fy0 != y0 && fx1 != x1 && fy1 != y1 &&
             fabs(fx1 - fx0) + fabs(fy1 - fy0) <= 1.0) {
             if (fx0 >= 0.0 && fx0 < W && fy0 >= 0.0 && fy0 < H) {
-                sink((long long)fy0 * W + (long long)fx0);
+                sink((long long)fy0 * W + (long long)fx0, (int)fx0, (int)fy0);
                 marks++;
             }
             if ((fx1 != fx0 || fy1 != fy0) && fx1 >= 0.0 && fx1 < W && fy1 >= 0.0 && fy1 < H) {
-                sink((long long)fy1 * W + (long long)fx1);
+                sink((long long)fy1 * W + (long long)fx1, (int)fx1, (int)fy1);
                 marks++;
             }
             return 0;

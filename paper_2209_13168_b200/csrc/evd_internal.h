@@ -129,7 +129,7 @@ void launch_frontier(const double *xc, const double *yc, const double *t, long l
                      const double *lo, const double *hi, const double *den_lo,
                      const double *den_hi, int K, double cx, double cy, int W, int H,
                      unsigned int *images, long long M, unsigned long long *fi_out,
-                     unsigned long long *marks_s, cudaStream_t s);
+                     unsigned long long *marks_s, bool exact_only, cudaStream_t s);
 constexpr int kFrontGroupHost = 32;
 void launch_image_sums(const unsigned int *img, long long m, unsigned long long *acc,
                        cudaStream_t s);
@@ -173,5 +173,26 @@ cudaError_t launch_event_probe(const double *xc, const double *yc, const double 
                                const double *nu3, const double *den3, double cx, double cy,
                                int W, int H, int blocks, int reps, unsigned long long *ctrs,
                                unsigned long long *span, unsigned int *scratch, cudaStream_t s);
+
+// ---- tiled batched frontier (evd_frontier_tiles.cu) ----
+struct FrontierTiles;
+FrontierTiles *tiles_new();
+void tiles_free(FrontierTiles *f);
+// Bin the resident window (centred events) into the frame's angular tiles,
+// once per window generation `gen`.  *usable = false when the tiled path does
+// not apply to this window (frame not tileable, non-finite events, a tile
+// listing more events than its u16 counters allow).
+cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, const double *t,
+                      long long n, int W, int H, unsigned long long gen, bool *usable,
+                      int *launches, cudaStream_t s);
+// bound_terms for K intervals (every hi <= 0) over the binned window:
+// fi_out[k] += fully_inside, marks_s[2k] += sum(H), marks_s[2k+1] += sum(H^2).
+cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, const double *dlo,
+                       const double *dhi, int K, unsigned long long *fi_out,
+                       unsigned long long *marks_s, int *launches, cudaStream_t s);
+// out[0] tiles (0: frame not tiled), out[1] pixels per tile (max), out[2]
+// listed events of the binned window (-1: not binned / not usable), out[3]
+// tiles with work
+void tiles_info(const FrontierTiles *f, long long *out);
 
 }  // namespace evd

@@ -79,7 +79,7 @@ static int event_blocks(long long n)
 // explicit red.global keeps every mark a RED.
 struct AtomicSink {
     unsigned int *img;
-    __device__ __forceinline__ void operator()(long long p) const
+    __device__ __forceinline__ void operator()(long long p, int, int) const
     {
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(img + p));
     }
@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(kThreads) k_frontier_f(
             long long pix, pix2;
             int ins;
             if (sure_segment_adj(aq, bq, ma, mb, W, H, pix, pix2, ins)) {
-                if (pix >= 0) sink(pix);
-                if (pix2 >= 0) sink(pix2);
+                if (pix >= 0) sink(pix, 0, 0);
+                if (pix2 >= 0) sink(pix2, 0, 0);
                 fi += ins;
             } else {
                 unc = true;
@@ -547,7 +547,7 @@ __global__ void k_raster_segments(const double *__restrict__ segs, int k, int W,
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= k) return;
     unsigned int *img = counts + (long long)j * W * H;
-    auto sink = [img](long long p) { img[p] += 1u; };
+    auto sink = [img](long long p, int, int) { img[p] += 1u; };
     raster_segment(segs[4 * j], segs[4 * j + 1], segs[4 * j + 2], segs[4 * j + 3], W, H, chunk,
                    sink);
 }
@@ -2052,14 +2052,13 @@ void launch_frontier(const double *xc, const double *yc, const double *t, long l
                      const double *lo, const double *hi, const double *den_lo,
                      const double *den_hi, int K, double cx, double cy, int W, int H,
                      unsigned int *images, long long M, unsigned long long *fi_out,
-                     unsigned long long *marks_s, cudaStream_t s)
+                     unsigned long long *marks_s, bool exact_only, cudaStream_t s)
 {
     set_attrs();
     const int groups = (K + kFrontGroup - 1) / kFrontGroup;
     long long bpg = (n + kThreads - 1) / kThreads;
     if (bpg > (long long)num_sms() * EVD_FRONT_BPG) bpg = (long long)num_sms() * EVD_FRONT_BPG;
     if (bpg < 1) bpg = 1;
-    static const bool exact_only = getenv("EVD_FRONTIER_FILTER") && getenv("EVD_FRONTIER_FILTER")[0] == '0';
     if (exact_only)
         k_frontier<<<(unsigned)(groups * bpg), kThreads, kBoundSmem, s>>>(
             xc, yc, t, n, lo, hi, den_lo, den_hi, K, cx, cy, W, H, images, M, (int)bpg, fi_out);

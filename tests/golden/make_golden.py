@@ -430,7 +430,8 @@ def make_preproc():
 # ------------------------------------------------------------------ synth
 def make_synth():
     out = {}
-    for cfg, (w, h, npts, sp) in {1: (240, 180, 1450, 1.0), 2: (346, 260, 10000, 1.0)}.items():
+    for cfg, (w, h, npts, sp) in {1: (240, 180, 1450, 1.0), 2: (346, 260, 10000, 1.0),
+                                  3: (640, 480, 13000, 0.5), 5: (1280, 720, 38000, 0.5)}.items():
         stream, _ = generate_landing_events(SimConfig(
             z0=1.0, nu=-0.4, geometry=SensorGeometry(w, h), duration=2.0, n_points=npts,
             event_spacing_px=sp, seed=0))
@@ -439,6 +440,60 @@ def make_synth():
         out[str(cfg)] = {"n": b.n, "sha256": hsh, "stream_n": stream.n}
     with open(os.path.join(HERE, "synth.json"), "w") as fh:
         json.dump(out, fh, indent=1)
+
+
+# ------------------------------------------------------------------ cfg-3 frontier
+def _frontier_leaf(args):
+    """bound_terms (contrast.py:241-251) of one leaf, run by the reference's own
+    numba kernel; also the mark total (upper_bound_image().in_image_events)."""
+    j, lo, hi = args
+    from eventdiv.geometry import VelocityInterval
+    b = _FRONTIER_BATCH
+    g = b.geometry
+    x0, y0, x1, y1 = con._segment_endpoints(b, VelocityInterval(lo, hi))
+    counts = np.zeros((g.height, g.width), dtype=np.float64)
+    stamp = np.full((g.height, g.width), -1, dtype=np.int64)
+    fi = con._bound_image_kernel(x0, y0, x1, y1, g.width, g.height, counts, stamp)
+    bound = con.bound_terms(b, VelocityInterval(lo, hi)) if j % 512 == 0 else None
+    s_bar = float(np.sum(counts**2))
+    if bound is not None:  # the public entry point agrees with the kernel call above
+        assert bound.s_bar == s_bar and bound.mu_lower == fi / g.n_pixels
+    return j, s_bar, int(fi), float(counts.sum())
+
+
+_FRONTIER_BATCH = None
+
+
+def make_frontier(procs: int = 8):
+    """The SURVEY §8(d) cfg-3 frontier: all 4096 depth-12 leaves of the root
+    bisection of the 640x480, 999,557-event window, each bound evaluated by the
+    reference (one numba _bound_image_kernel per leaf, leaves spread over
+    `procs` worker processes).  The window is the reference simulator's own."""
+    global _FRONTIER_BATCH
+    import multiprocessing as mp
+    from eventdiv.geometry import velocity_domain
+    stream, _ = generate_landing_events(SimConfig(
+        z0=1.0, nu=-0.4, geometry=SensorGeometry(640, 480), duration=2.0, n_points=13000,
+        event_spacing_px=0.5, seed=0))
+    _FRONTIER_BATCH = batch_stream(stream, 0.5)[0]
+    level = [velocity_domain(0.5)]
+    for _ in range(12):
+        level = [c for iv in level for c in iv.split()]
+    jobs = [(j, iv.lo, iv.hi) for j, iv in enumerate(level)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        rows = sorted(pool.map(_frontier_leaf, jobs, chunksize=16))
+    s_bar = np.array([r[1] for r in rows], dtype=np.float64)
+    fi = np.array([r[2] for r in rows], dtype=np.int64)
+    marks = np.array([r[3] for r in rows], dtype=np.float64)
+    assert np.all(s_bar < 2.0**53) and np.all(marks < 2.0**53)  # exact integers
+    hsh = hashlib.sha256(_FRONTIER_BATCH.x.tobytes() + _FRONTIER_BATCH.y.tobytes() +
+                         _FRONTIER_BATCH.t.tobytes()).hexdigest()
+    np.savez_compressed(os.path.join(HERE, "frontier_cfg3.npz"),
+                        lo=np.array([r[1] for r in jobs]), hi=np.array([r[2] for r in jobs]),
+                        s_bar=s_bar.astype(np.uint64), fully_inside=fi,
+                        marks=marks.astype(np.uint64),
+                        window_sha256=np.frombuffer(hsh.encode(), np.uint8))
+    print("frontier: 4096 leaves, marks", int(marks.sum()))
 
 
 def make_nonfinite():
@@ -510,3 +565,5 @@ if __name__ == "__main__":
         make_bnb(big)
     if "nonfinite" in what:
         make_nonfinite()
+    if "frontier" in what:
+        make_frontier()

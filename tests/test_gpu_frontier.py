@@ -1,7 +1,11 @@
 """Batched frontier (one launch for many intervals) == per-interval bounds (GPU)."""
 
+import os
+
 import numpy as np
 import pytest
+
+from conftest import GOLDEN
 
 from oracle import oracle as orc
 import paper_2209_13168_b200 as evd
@@ -45,6 +49,136 @@ def test_frontier_bounds_assembly_bits():
     cb = fr.frontier_bounds(b, lo, hi)
     for j in range(0, 64, 7):
         assert cb[j] == evd.bound_terms(b, VelocityInterval(lo[j], hi[j])).c_bar
+
+
+@pytest.fixture
+def frontier_path():
+    """Set the context's frontier path for one test; back to auto afterwards."""
+    from paper_2209_13168_b200 import _lib
+    ctx = _lib.context()
+    yield ctx
+    ctx.set_option("frontier_path", _lib.FRONTIER_AUTO)
+    ctx.set_option("frontier_image_budget", 8 << 30)
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    b = synth.config_window(3)
+    assert b.n == 999557
+    lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
+    g = np.load(os.path.join(GOLDEN, "frontier_cfg3.npz"))
+    assert np.array_equal(lo, g["lo"]) and np.array_equal(hi, g["hi"])
+    return b, lo, hi, g
+
+
+@pytest.mark.parametrize("path,budget", [("tiles", None), ("global", None),
+                                         ("global_exact", None), ("global", 1000 * 307200 * 4)])
+def test_cfg3_frontier_all_leaves_vs_reference(cfg3, frontier_path, path, budget):
+    """BASELINE configs[2]: all 4096 depth-12 leaves of the 999,557-event
+    640x480 window in one evd_eval_frontier call, every leaf's (S_bar,
+    fully_inside, marks) equal to the reference's own bound_terms
+    (tests/golden/frontier_cfg3.npz, numba kernel per leaf).  Every path: the
+    on-chip tiles, the global-image filtered kernel, its exact-only variant,
+    and the global path chunked (image budget of 1000 intervals -> 4 launches)."""
+    from paper_2209_13168_b200 import _lib
+    b, lo, hi, g = cfg3
+    ctx = frontier_path
+    code = {"tiles": _lib.FRONTIER_TILES, "global": _lib.FRONTIER_GLOBAL,
+            "global_exact": _lib.FRONTIER_GLOBAL_EXACT}[path]
+    ctx.set_option("frontier_path", code)
+    if budget:
+        ctx.set_option("frontier_image_budget", budget)
+    s, fi, mk = con.frontier_terms(b, lo, hi, ctx=ctx)
+    assert ctx.frontier_info()["last_path"] == code
+    assert np.array_equal(fi, g["fully_inside"])
+    assert np.array_equal(mk, g["marks"])
+    assert np.array_equal(s, g["s_bar"])
+    assert int(mk.sum()) == 1787442891
+
+
+def test_cfg3_bound_images_all_leaves_vs_reference(cfg3):
+    """The per-interval kernel (k_bound_image, evd_bound_images) on all 4096
+    leaves against the same reference golden: an independent second device
+    path for every leaf."""
+    b, lo, hi, g = cfg3
+    s, fi, mk, _ = con.bound_terms_many(b, lo, hi)
+    assert np.array_equal(fi, g["fully_inside"]) and np.array_equal(mk, g["marks"])
+    assert np.array_equal(s, g["s_bar"])
+
+
+def _paths_agree(ctx, b, lo, hi):
+    from paper_2209_13168_b200 import _lib
+    out = {}
+    for code in (_lib.FRONTIER_TILES, _lib.FRONTIER_GLOBAL):
+        ctx.set_option("frontier_path", code)
+        out[code] = con.frontier_terms(b, lo, hi, ctx=ctx)
+        assert ctx.frontier_info()["last_path"] == code
+    for a, c in zip(out[_lib.FRONTIER_TILES], out[_lib.FRONTIER_GLOBAL]):
+        assert np.array_equal(a, c)
+    return out[_lib.FRONTIER_TILES]
+
+
+@pytest.mark.parametrize("w,h,n", [(64, 48, 3000), (65, 49, 5000), (240, 180, 20000),
+                                   (347, 261, 60000), (31, 7, 800), (1280, 720, 200000)])
+def test_tiled_frontier_equals_global_random(frontier_path, w, h, n):
+    """Tiled (shared-memory) frontier == global-image frontier on uniform
+    windows: odd / even frames (FOE on a pixel centre or corner), frames
+    smaller than one tile, random intervals of every width in the domain,
+    the root, adjacent leaves and singletons."""
+    r = np.random.default_rng(w * 1000 + h)
+    b = synth.random_window(r, w, h, n)
+    dom = velocity_domain(b.tau)
+    llo, lhi = fr.uniform_frontier(dom, 6)
+    rl, rh = np.sort(r.uniform(dom.lo, dom.hi, (2, 70)), axis=0)
+    sing = r.uniform(dom.lo, dom.hi, 5)
+    lo = np.concatenate([llo, rl, [dom.lo], sing, [0.0]])
+    hi = np.concatenate([lhi, rh, [dom.hi], sing, [0.0]])
+    s, fi, mk = _paths_agree(frontier_path, b, lo, hi)
+    assert int(mk.sum()) > 0
+
+
+def test_tiled_frontier_landing_windows(frontier_path):
+    """Structured windows (radial trajectories, events at the FOE, t = tau):
+    cfg 1 and the cfg-2 window against the global path on a depth-8 frontier."""
+    for cfg in (1, 2):
+        b = synth.config_window(cfg)
+        lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 8)
+        _paths_agree(frontier_path, b, lo, hi)
+    # events exactly at the FOE and on the FOE's row / column, t = 0 and t = tau
+    w, h = 64, 48
+    x = np.array([32.0, 32.0, 0.0, 63.9, 32.0, 31.5, 32.5, 10.0, 32.0])
+    y = np.array([24.0, 24.0, 24.0, 24.0, 0.0, 24.0, 24.0, 10.0, 47.99])
+    t = np.array([0.0, 0.5, 0.1, 0.2, 0.3, 0.25, 0.5, 0.5, 0.4])
+    b = evd.EventBatch(x, y, t, 0.5, evd.SensorGeometry(w, h))
+    lo, hi = fr.uniform_frontier(velocity_domain(0.5), 7)
+    _paths_agree(frontier_path, b, lo, hi)
+
+
+def test_tiled_frontier_fallbacks(frontier_path):
+    """Auto takes the global path where tiles do not apply (nu > 0, non-finite
+    events); forcing tiles there fails loudly."""
+    from paper_2209_13168_b200 import _lib
+    ctx = frontier_path
+    r = np.random.default_rng(3)
+    b = synth.random_window(r, 64, 48, 2000)
+    lo, hi = np.array([-0.5, -0.1, 0.0]), np.array([-0.1, 0.2, 0.3])   # nu > 0
+    a = con.frontier_terms(b, lo, hi, ctx=ctx)
+    assert ctx.frontier_info()["last_path"] == _lib.FRONTIER_GLOBAL
+    c = con.bound_terms_many(b, lo, hi, ctx=ctx)
+    assert all(np.array_equal(u, v) for u, v in zip(a, c[:3]))
+    ctx.set_option("frontier_path", _lib.FRONTIER_TILES)
+    with pytest.raises(_lib.EvdError):
+        con.frontier_terms(b, lo, hi, ctx=ctx)
+    x = b.x.copy()
+    x[7] = np.nan
+    bn = evd.EventBatch(x, b.y, b.t, b.tau, b.geometry)
+    with pytest.raises(_lib.EvdError):
+        con.frontier_terms(bn, [-0.5], [-0.1], ctx=ctx)
+    ctx.set_option("frontier_path", _lib.FRONTIER_AUTO)
+    a = con.frontier_terms(bn, [-0.5, -1.0], [-0.1, -0.5], ctx=ctx)
+    assert ctx.frontier_info()["last_path"] == _lib.FRONTIER_GLOBAL
+    c = con.bound_terms_many(bn, [-0.5, -1.0], [-0.1, -0.5], ctx=ctx)
+    assert all(np.array_equal(u, v) for u, v in zip(a, c[:3]))
 
 
 def test_cfg3_frontier_sample_vs_oracle():

@@ -134,3 +134,26 @@ def test_preprocessing_oracle_matches_reference():
         n = c["name"]
         rx, ry = orc.rescale(z[f"{n}_x"], z[f"{n}_y"], c["w"], c["h"], c["w2"], c["h2"])
         assert np.array_equal(rx, z[f"{n}_rx"]) and np.array_equal(ry, z[f"{n}_ry"])
+
+
+def test_cfg3_frontier_golden_sample():
+    """frontier_cfg3.npz holds the reference's own bound of all 4096 depth-12
+    leaves of the 999,557-event cfg-3 window (make_golden.py frontier); the
+    leaves are the bisection's endpoints, and the oracle agrees on a sample."""
+    from paper_2209_13168_b200 import frontier as fr, synth
+    from paper_2209_13168_b200.geometry import velocity_domain
+    g = np.load(os.path.join(GOLDEN, "frontier_cfg3.npz"))
+    lo, hi = fr.uniform_frontier(velocity_domain(0.5), 12)
+    assert np.array_equal(lo, g["lo"]) and np.array_equal(hi, g["hi"])
+    assert int(g["marks"].sum()) == 1787442891
+    b = synth.config_window(3)
+    orc.THREADS = os.cpu_count() or 1
+    try:
+        for j in (0, 700, 1500, 2600, 3300, 4095):
+            counts, fi = orc.bound_image(b, lo[j], hi[j])
+            c = counts.astype(np.uint64)
+            assert fi == int(g["fully_inside"][j]), j
+            assert int(c.sum()) == int(g["marks"][j]), j
+            assert int((c * c).sum()) == int(g["s_bar"][j]), j
+    finally:
+        orc.THREADS = 1

@@ -1,7 +1,8 @@
 """Throughput of the batched frontier (config 3: 640x480 window, 999,557 events,
 the 4096 depth-12 leaves of the root bisection in one evd_eval_frontier call).
 
-python tools/bench_frontier.py [reps]   -> one JSON line
+python tools/bench_frontier.py [reps] [path]   -> one JSON line
+path: auto (default) | tiles | global | global_exact (evd_set_option "frontier_path")
 """
 
 import json
@@ -24,6 +25,8 @@ def main():
     b = synth.config_window(3)
     lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
     ctx = _lib.context()
+    path = sys.argv[2] if len(sys.argv) > 2 else "auto"
+    ctx.set_option("frontier_path", {"auto": 0, "tiles": 1, "global": 2, "global_exact": 3}[path])
     stream = torch.cuda.Stream()  # explicit: handle 0 would mean the context's own stream
     torch.cuda.set_stream(stream)
     ctx.lib.evd_set_stream(ctx.h, _lib._vp(stream.cuda_stream))
@@ -56,7 +59,7 @@ def main():
         "marks": marks, "marks_per_event_interval": marks / units,
         "atomics_per_s": marks / t, "atomic_peak": apk,
         "atomic_frac": (marks / t / 1e9 / apk) if apk else None,
-        "launches_per_call": launches,
+        "launches_per_call": launches, "path": path, "info": ctx.frontier_info(),
         "hbm_alg_bytes": 24 * b.n, "note": "events read once per call (24 B/event)",
     }))
 
