@@ -98,6 +98,8 @@ struct FrontierTiles {
     size_t flag_cap = 0;
     double *xs = nullptr, *ys = nullptr, *ts = nullptr;
     size_t xs_cap = 0, ys_cap = 0, ts_cap = 0;
+    float *rho = nullptr;           // per listed event: frame-exit scale (see k_tile_fill)
+    size_t rho_cap = 0;
     int *order = nullptr;           // tiles with work, heaviest list first
     size_t order_cap = 0;
     int n_order = 0;
@@ -113,7 +115,8 @@ void tiles_free(FrontierTiles *f)
     if (!f) return;
     for (void *p : {(void *)f->meta, (void *)f->rows, (void *)f->ang, (void *)f->start,
                     (void *)f->cnt, (void *)f->cursor, (void *)f->flag, (void *)f->xs,
-                    (void *)f->ys, (void *)f->ts, (void *)f->order, (void *)f->ctr})
+                    (void *)f->ys, (void *)f->ts, (void *)f->rho, (void *)f->order,
+                    (void *)f->ctr})
         if (p) cudaFree(p);
     delete f;
 }
@@ -322,52 +325,68 @@ __global__ void k_tile_count(const double *__restrict__ xc, const double *__rest
         if (hist[i]) atomicAdd((i & 1) ? &cnt[i >> 1].y : &cnt[i >> 1].x, hist[i]);
 }
 
-// cursor[2k] / [2k+1]: next home / foreign slot of tile k
+// cursor[2k] / [2k+1]: next home / foreign slot of tile k.  rho (rounded up
+// to float) is the event's frame-exit scale: the ray from the FOE through the
+// event leaves the closed frame at distance min(cx/|ux|, cy/|uy|) (unit
+// direction u), so every point of it at scale s > rho = min(cx/|xc|, cy/|yc|)
+// + 1.5/|x - c| lies more than 1.5 px beyond the frame.
 __global__ void k_tile_fill(const double *__restrict__ xc, const double *__restrict__ yc,
-                            const double *__restrict__ t, long long n, TileGeom g,
-                            unsigned long long *cursor, double *xs, double *ys, double *ts)
+                            const double *__restrict__ t, long long n, TileGeom g, double cx,
+                            double cy, unsigned long long *cursor, double *xs, double *ys,
+                            double *ts, float *rho)
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double x = xc[i], y = yc[i], tt = t[i];
+        const double r = hypot(x, y);
+        const float q = r > 0.0 ? __double2float_ru(fmin(cx / fabs(x), cy / fabs(y)) + 1.5 / r)
+                                : INFINITY;
         for_each_tile(x, y, g, [&](int k, bool home) {
             const unsigned long long p = atomicAdd(cursor + 2 * k + (home ? 0 : 1), 1ull);
             xs[p] = x;
             ys[p] = y;
             ts[p] = tt;
+            rho[p] = q;
         });
     }
 }
 
 // ---------------------------------------------------------------- tile kernel
 // Marks of one interval's image restricted to the tile: (x, y) -> local pixel
-// through the tile's row table, u16 counters packed in pairs.
+// through the tile's row table (two runs per row), u16 counters packed in
+// pairs.  Shared-window addresses are 32-bit.
 struct TileSink {
-    unsigned int *img;
-    const int4 *rows;
+    unsigned img;    // shared address of this interval's image
+    unsigned rows;   // shared address of the row table (int4 per row)
     int y0, nrows;
     __device__ __forceinline__ void operator()(long long, int x, int y) const
     {
         const int r = y - y0;
         if ((unsigned)r < (unsigned)nrows) {
-            const int4 e = rows[r];
-            const int xl = e.x & 0xffff, xh = (int)((unsigned)e.x >> 16);
-            const int xl2 = e.z & 0xffff, xh2 = (int)((unsigned)e.z >> 16);
+            int e0, e1, e2, e3;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+                         : "r"(rows + 16u * (unsigned)r));
+            const int xl = e0 & 0xffff, xh = (int)((unsigned)e0 >> 16);
+            const int xl2 = e2 & 0xffff, xh2 = (int)((unsigned)e2 >> 16);
             int l = -1;
-            if (x >= xl && x <= xh) l = e.y + x - xl;
-            else if (x >= xl2 && x <= xh2) l = e.w + x - xl2;
-            if (l >= 0) atomicAdd(img + (l >> 1), 1u << ((l & 1) << 4));
+            if (x >= xl && x <= xh) l = e1 + x - xl;
+            else if (x >= xl2 && x <= xh2) l = e3 + x - xl2;
+            if (l >= 0)
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(img + 4u * (unsigned)(l >> 1)),
+                             "r"(1u << ((l & 1) << 4))
+                             : "memory");
         }
     }
 };
 
 struct TileView {
-    unsigned int *img;  // 32 images, `words` apart
-    const int4 *rows;
+    unsigned img;    // shared address of image 0; image j at img + 4 * j * words
+    unsigned rows;
     int y0, nrows, words;
     __device__ __forceinline__ TileSink sink(int j) const
     {
-        return TileSink{img + j * words, rows, y0, nrows};
+        return TileSink{img + 4u * (unsigned)(j * words), rows, y0, nrows};
     }
 };
 
@@ -443,6 +462,7 @@ __device__ __forceinline__ bool sure_cells(const Warped &a, const Warped &b, dou
 
 struct TileArgs {
     const double *xs, *ys, *ts;  // listed events, tile-major
+    const float *rho;            // their frame-exit scales
     const long long *start;
     const int2 *cnt;             // (home, all)
     const int4 *meta;
@@ -455,6 +475,60 @@ struct TileArgs {
     unsigned int *ctr;
     unsigned long long *fi_out, *marks_s;
 };
+
+// One work item's state the out-of-line exact path needs.
+struct TileItem {
+    const double *xs, *ys, *ts;
+    long long e0;
+    int n_home;
+    double lo, hi, dlo, dhi;   // this lane's interval
+    double cx, cy;
+    int W, H;
+    TileView view;
+};
+
+// The exact path (reference arithmetic) for the last `take` uncertain pairs
+// queued in q.ev: lanes take one pair each; fully_inside of home events into
+// s_fi; multi-pixel segments queued and drained 32 at a time.  Returns the
+// new queued-segment count.
+__device__ __noinline__ int tile_exact(TileQueue &q, int nx, int take, int nq,
+                                       const TileItem &it, unsigned long long *s_fi)
+{
+    const int lane = threadIdx.x & 31;
+    const int code = lane < take ? q.ev[nx - take + lane] : -1;
+    __syncwarp();
+    const int j = code >= 0 ? (code & 31) : 0;
+    const double lo_j = __shfl_sync(0xffffffffu, it.lo, j);
+    const double hi_j = __shfl_sync(0xffffffffu, it.hi, j);
+    const double dlo_j = __shfl_sync(0xffffffffu, it.dlo, j);
+    const double dhi_j = __shfl_sync(0xffffffffu, it.dhi, j);
+    TileSink sj = it.view.sink(j);
+    SegDesc d;
+    int c = 0, mk = 0;
+    if (code >= 0) {
+        const int el = code >> 5;
+        const long long e = it.e0 + el;
+        const double x = __ldg(it.xs + e), y = __ldg(it.ys + e), tt = __ldg(it.ts + e);
+        const Warped wa = warp_event(x, y, tt, lo_j, dlo_j, it.cx, it.cy);
+        const Warped wb = warp_event(x, y, tt, hi_j, dhi_j, it.cx, it.cy);
+        if (el < it.n_home && fully_inside(wa.x, wa.y, wb.x, wb.y, it.W, it.H))
+            atomicAdd(s_fi + j, 1ull);
+        c = build_segment(wa.x, wa.y, wb.x, wb.y, it.W, it.H, 16, d, sj, mk);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
+    if (c > 0) {
+        const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+        q.d[slot] = d;
+        q.jj[slot] = (unsigned char)j;
+    }
+    nq += __popc(bal);
+    if (nq >= 32) {
+        __syncwarp();
+        tile_drain(q, nq, it.W, it.H, it.view);
+        nq = 0;
+    }
+    return nq;
+}
 
 __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
 {
@@ -471,6 +545,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
     const int W = a.W, H = a.H;
     const double cx = a.cx, cy = a.cy;
     const long long items = (long long)a.n_order * a.groups;
+    const unsigned img_s = (unsigned)__cvta_generic_to_shared(img);
+    const unsigned rows_s = (unsigned)__cvta_generic_to_shared(rows);
     for (;;) {
         if (threadIdx.x == 0) s_item = (int)atomicAdd(a.ctr, 1u);
         if (threadIdx.x < 32) s_fi[threadIdx.x] = 0ull;
@@ -481,95 +557,113 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         const int4 m = a.meta[tile];
         for (int i = threadIdx.x; i < m.y; i += blockDim.x) rows[i] = a.rows[m.z + i];
         __syncthreads();
-        const TileView view{img, rows, m.x, m.y, words};
-        const long long e0 = a.start[tile];
+        TileItem it;
+        it.view = TileView{img_s, rows_s, m.x, m.y, words};
+        it.xs = a.xs;
+        it.ys = a.ys;
+        it.ts = a.ts;
+        it.e0 = a.start[tile];
         const int2 cn = a.cnt[tile];
+        it.n_home = cn.x;
+        it.cx = cx;
+        it.cy = cy;
+        it.W = W;
+        it.H = H;
         // lane j evaluates interval g*32 + j
         const int k = g * 32 + lane;
         const bool valid = k < a.K;
         const int kc = valid ? k : a.K - 1;
-        const double my_lo = __ldg(a.lo + kc), my_hi = __ldg(a.hi + kc);
-        const double my_dlo = __ldg(a.den_lo + kc), my_dhi = __ldg(a.den_hi + kc);
-        const double my_rlo = ddiv(1.0, my_dlo), my_rhi = ddiv(1.0, my_dhi);
-        const double left_hi = __shfl_up_sync(0xffffffffu, my_hi, 1);
-        const bool shared_lo = lane > 0 && my_lo == left_hi;
-        const TileSink my_sink = view.sink(lane);
+        it.lo = __ldg(a.lo + kc);
+        it.hi = __ldg(a.hi + kc);
+        it.dlo = __ldg(a.den_lo + kc);
+        it.dhi = __ldg(a.den_hi + kc);
+        const double my_rlo = ddiv(1.0, it.dlo), my_rhi = ddiv(1.0, it.dhi);
+        const double left_hi = __shfl_up_sync(0xffffffffu, it.hi, 1);
+        const bool shared_lo = lane > 0 && it.lo == left_hi;
+        // Whole-group rejection: the scale s(nu, t) = (1 + nu t) / (1 + nu tau)
+        // decreases in nu (ds/dnu = (t - tau) / den^2 <= 0), so every endpoint
+        // of the group's segments lies at scale >= s(hmax, t) along the
+        // event's ray; beyond the frame-exit scale rho (+1.5 px) no sample of
+        // any of them can touch an in-frame pixel (and none is fully inside).
+        // Relative errors here are ~1e-15, the slack 1e-9; rounding in the
+        // reference's clip is < 1e-3 px while |x'| < 1e12 (kappa).
+        double hmax = valid ? it.hi : -INFINITY, rhmax = my_rhi;
+        double smax = valid ? my_rlo : 0.0;  // s(lo, 0) = 1 / den(lo): the largest scale
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double h2 = __shfl_xor_sync(0xffffffffu, hmax, o);
+            const double r2 = __shfl_xor_sync(0xffffffffu, rhmax, o);
+            if (h2 > hmax || (h2 == hmax && r2 > rhmax)) { hmax = h2; rhmax = r2; }
+            smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        }
+        const double kappa = smax * (hypot(cx, cy) + 1.5) * 1e-12;
+        const TileSink my_sink = it.view.sink(lane);
         unsigned long long fi = 0;
         int nq = 0, nx = 0;  // queued segments / uncertain pairs (warp-uniform)
-        auto exact_batch = [&](int take) {
-            const int code = lane < take ? wq.ev[nx - take + lane] : -1;
-            nx -= take;
-            __syncwarp();
-            const int j = code >= 0 ? (code & 31) : 0;
-            const double lo_j = __shfl_sync(0xffffffffu, my_lo, j);
-            const double hi_j = __shfl_sync(0xffffffffu, my_hi, j);
-            const double dlo_j = __shfl_sync(0xffffffffu, my_dlo, j);
-            const double dhi_j = __shfl_sync(0xffffffffu, my_dhi, j);
-            TileSink sj = view.sink(j);
-            SegDesc d;
-            int c = 0, mk = 0;
-            if (code >= 0) {
-                const int el = code >> 5;
-                const long long e = e0 + el;
-                const double x = __ldg(a.xs + e), y = __ldg(a.ys + e), tt = __ldg(a.ts + e);
-                const Warped wa = warp_event(x, y, tt, lo_j, dlo_j, cx, cy);
-                const Warped wb = warp_event(x, y, tt, hi_j, dhi_j, cx, cy);
-                if (el < cn.x && fully_inside(wa.x, wa.y, wb.x, wb.y, W, H))
-                    atomicAdd(s_fi + j, 1ull);
-                c = build_segment(wa.x, wa.y, wb.x, wb.y, W, H, 16, d, sj, mk);
+        // Events in chunks of 32: lane l loads event l of the chunk (coalesced),
+        // tests the whole-group rejection for it, and the warp then walks only
+        // the surviving events, broadcasting each from its lane.
+        for (int c0 = warp * 32; c0 < cn.y; c0 += kTileWarps * 32) {
+            const int el_l = c0 + lane;
+            double xl = 0.0, yl = 0.0, tl = 0.0;
+            bool need = false;
+            if (el_l < cn.y) {
+                const long long e = it.e0 + el_l;
+                tl = __ldg(a.ts + e);
+                xl = __ldg(a.xs + e);
+                yl = __ldg(a.ys + e);
+                const double rho = (double)__ldg(a.rho + e);
+                const double smin = dmul(dadd(1.0, dmul(hmax, tl)), rhmax);
+                need = !(smin > rho * (1.0 + 1e-9) && rho > kappa);
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
-            if (c > 0) {
-                const int slot = nq + __popc(bal & ((1u << lane) - 1u));
-                wq.d[slot] = d;
-                wq.jj[slot] = (unsigned char)j;
-            }
-            nq += __popc(bal);
-            if (nq >= 32) {
-                __syncwarp();
-                tile_drain(wq, nq, W, H, view);
-                nq = 0;
-            }
-        };
-        for (int el = warp; el < cn.y; el += kTileWarps) {
-            const long long e = e0 + el;
-            const double x = __ldg(a.xs + e), y = __ldg(a.ys + e), tt = __ldg(a.ts + e);
-            const Warped bq = warp_approx(x, y, tt, my_hi, my_rhi, cx, cy);
-            const double mb = sure_margin(bq, cx, cy);
-            Warped aq;
-            aq.x = __shfl_up_sync(0xffffffffu, bq.x, 1);
-            aq.y = __shfl_up_sync(0xffffffffu, bq.y, 1);
-            double ma = __shfl_up_sync(0xffffffffu, mb, 1);
-            if (!shared_lo) {
-                aq = warp_approx(x, y, tt, my_lo, my_rlo, cx, cy);
-                ma = sure_margin(aq, cx, cy);
-            }
-            bool unc = false;
-            if (valid) {
-                int xa, ya, xb, yb, ins;
-                if (sure_cells(aq, bq, ma, mb, W, H, xa, ya, xb, yb, ins)) {
-                    if (xa >= 0) my_sink(0, xa, ya);
-                    if (xb >= 0) my_sink(0, xb, yb);
-                    if (el < cn.x) fi += ins;
-                } else {
-                    unc = true;
+            unsigned todo = __ballot_sync(0xffffffffu, need);
+            while (todo) {
+                const int i = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int el = c0 + i;
+                const double x = __shfl_sync(0xffffffffu, xl, i);
+                const double y = __shfl_sync(0xffffffffu, yl, i);
+                const double tt = __shfl_sync(0xffffffffu, tl, i);
+                const Warped bq = warp_approx(x, y, tt, it.hi, my_rhi, cx, cy);
+                const double mb = sure_margin(bq, cx, cy);
+                Warped aq;
+                aq.x = __shfl_up_sync(0xffffffffu, bq.x, 1);
+                aq.y = __shfl_up_sync(0xffffffffu, bq.y, 1);
+                double ma = __shfl_up_sync(0xffffffffu, mb, 1);
+                if (!shared_lo) {
+                    aq = warp_approx(x, y, tt, it.lo, my_rlo, cx, cy);
+                    ma = sure_margin(aq, cx, cy);
                 }
-            }
-            const unsigned bu = __ballot_sync(0xffffffffu, unc);
-            if (unc) wq.ev[nx + __popc(bu & ((1u << lane) - 1u))] = (el << 5) | lane;
-            nx += __popc(bu);
-            if (nx >= 32) {
-                __syncwarp();
-                exact_batch(32);
+                bool unc = false;
+                if (valid) {
+                    int xa, ya, xb, yb, ins;
+                    if (sure_cells(aq, bq, ma, mb, W, H, xa, ya, xb, yb, ins)) {
+                        if (xa >= 0) my_sink(0, xa, ya);
+                        if (xb >= 0) my_sink(0, xb, yb);
+                        if (el < cn.x) fi += ins;
+                    } else {
+                        unc = true;
+                    }
+                }
+                const unsigned bu = __ballot_sync(0xffffffffu, unc);
+                if (unc) wq.ev[nx + __popc(bu & ((1u << lane) - 1u))] = (el << 5) | lane;
+                nx += __popc(bu);
+                if (nx >= 32) {
+                    __syncwarp();
+                    nq = tile_exact(wq, nx, 32, nq, it, s_fi);
+                    nx -= 32;
+                }
             }
         }
         while (nx > 0) {
             __syncwarp();
-            exact_batch(nx < 32 ? nx : 32);
+            const int take = nx < 32 ? nx : 32;
+            nq = tile_exact(wq, nx, take, nq, it, s_fi);
+            nx -= take;
         }
         if (nq > 0) {
             __syncwarp();
-            tile_drain(wq, nq, W, H, view);
+            tile_drain(wq, nq, W, H, it.view);
         }
         if (valid && fi) atomicAdd(s_fi + lane, fi);
         __syncthreads();
@@ -685,7 +779,7 @@ cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, cons
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return f->h_cnt[a].y > f->h_cnt[b].y; });
     if ((e = ensure(f->xs, f->xs_cap, total)) || (e = ensure(f->ys, f->ys_cap, total)) ||
-        (e = ensure(f->ts, f->ts_cap, total)))
+        (e = ensure(f->ts, f->ts_cap, total)) || (e = ensure(f->rho, f->rho_cap, total)))
         return e;
     if ((e = cudaMemcpyAsync(f->start, start.data(), T * sizeof(long long), cudaMemcpyHostToDevice, s)) ||
         (e = cudaMemcpyAsync(f->cnt, f->h_cnt.data(), T * sizeof(int2), cudaMemcpyHostToDevice, s)) ||
@@ -695,7 +789,8 @@ cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, cons
                                                 cudaMemcpyHostToDevice, s))))
         return e;
     if (n > 0) {
-        k_tile_fill<<<blocks, 256, 0, s>>>(xc, yc, t, n, g, f->cursor, f->xs, f->ys, f->ts);
+        k_tile_fill<<<blocks, 256, 0, s>>>(xc, yc, t, n, g, W / 2.0, H / 2.0, f->cursor, f->xs,
+                                           f->ys, f->ts, f->rho);
         (*launches)++;
     }
     if ((e = cudaStreamSynchronize(s))) return e;  // host vectors above are freed on return
@@ -722,6 +817,7 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     a.xs = f->xs;
     a.ys = f->ys;
     a.ts = f->ts;
+    a.rho = f->rho;
     a.start = f->start;
     a.cnt = f->cnt;
     a.meta = f->meta;
