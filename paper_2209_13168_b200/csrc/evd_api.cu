@@ -727,6 +727,7 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
     const long long M = (long long)ctx->W * ctx->H;
     std::vector<double> host(4 * (size_t)k);
     bool nonpositive = true;  // every nu <= 0: the warp scale is >= 1 (tiled path)
+    bool contig = true;       // lo[j+1] == hi[j]: adjacent intervals share an endpoint warp
     for (int j = 0; j < k; j++) {
         if (lo[j] > hi[j]) return fail(ctx, EVD_ERR_ARG, "empty interval [%.17g, %.17g]", lo[j], hi[j]);
         if ((rc = check_den(ctx, lo[j], ctx->tau, &host[2 * (size_t)k + j]))) return rc;
@@ -734,6 +735,7 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
         host[j] = lo[j];
         host[(size_t)k + j] = hi[j];
         nonpositive = nonpositive && hi[j] <= 0.0;
+        if (j > 0 && lo[j] != hi[j - 1]) contig = false;
     }
     CU(cudaSetDevice(ctx->device));
     CU(ctx->fargs.ensure(4 * (size_t)k));
@@ -758,7 +760,8 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
                                         "tile over 65535 events)");
     if (tiled) {
         int nl = 0;
-        CU(tiles_eval(ctx->tiles, d_lo, d_hi, d_dl, d_dh, k, f_fi, f_ms, &nl, ctx->stream));
+        CU(tiles_eval(ctx->tiles, d_lo, d_hi, d_dl, d_dh, k, contig, f_fi, f_ms, &nl,
+                      ctx->stream));
         LAUNCHED(nl);
         ctx->last_frontier_path = EVD_FRONTIER_TILES;
     } else if (ctx->n > 0) {

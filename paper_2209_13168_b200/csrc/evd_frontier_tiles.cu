@@ -530,8 +530,98 @@ __device__ __noinline__ int tile_exact(TileQueue &q, int nx, int take, int nq,
     return nq;
 }
 
+// One endpoint warp of the filtered path: position, certification margin,
+// certified cell (code) and the cell's local index in the tile (or -1).
+// code = (fy + 2) << 16 | (fx + 2) when the exact position lies surely
+// strictly inside cell (fx, fy) with -2 <= fx, fy <= 32000, else kFar.
+constexpr unsigned kFar = 0xffffffffu;
+struct TilePoint {
+    double x, y, m;
+    unsigned code;
+    int l;
+};
+
+__device__ __forceinline__ int tile_local(const TileView &v, int x, int y)
+{
+    const int r = y - v.y0;
+    if ((unsigned)r >= (unsigned)v.nrows) return -1;
+    int e0, e1, e2, e3;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+                 : "r"(v.rows + 16u * (unsigned)r));
+    const int xl = e0 & 0xffff, xh = (int)((unsigned)e0 >> 16);
+    const int xl2 = e2 & 0xffff, xh2 = (int)((unsigned)e2 >> 16);
+    if (x >= xl && x <= xh) return e1 + x - xl;
+    if (x >= xl2 && x <= xh2) return e3 + x - xl2;
+    return -1;
+}
+
+__device__ __forceinline__ void tile_mark(unsigned img, int l)
+{
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(img + 4u * (unsigned)(l >> 1)),
+                 "r"(1u << ((l & 1) << 4))
+                 : "memory");
+}
+
+__device__ __forceinline__ TilePoint tile_point(double x, double y, double t, double nu,
+                                                double rden, double cx, double cy, int W, int H,
+                                                const TileView &v)
+{
+    TilePoint p;
+    const Warped w = warp_approx(x, y, t, nu, rden, cx, cy);
+    p.x = w.x;
+    p.y = w.y;
+    p.m = sure_margin(w, cx, cy);
+    const double fx = floor(w.x), fy = floor(w.y);
+    const bool sure = w.x - p.m > fx && w.x + p.m < fx + 1.0 && w.y - p.m > fy &&
+                      w.y + p.m < fy + 1.0 && fx >= -2.0 && fx <= 32000.0 && fy >= -2.0 &&
+                      fy <= 32000.0;
+    p.code = kFar;
+    p.l = -1;
+    if (sure) {
+        const int ix = (int)fx, iy = (int)fy;
+        p.code = ((unsigned)(iy + 2) << 16) | (unsigned)(ix + 2);
+        if (ix >= 0 && ix < W && iy >= 0 && iy < H) p.l = tile_local(v, ix, iy);
+    }
+    return p;
+}
+
+__device__ __forceinline__ bool code_in_frame(unsigned c, int W, int H)
+{
+    const int fx = (int)(c & 0xffffu) - 2, fy = (int)(c >> 16) - 2;
+    return fx >= 0 && fx < W && fy >= 0 && fy < H;
+}
+
+// Certified outcome of the segment a -> b (sure_segment_adj, evd_device.cuh,
+// from the points' certified cells): false if uncertain; else marks the
+// tile's pixels among the end cells and sets inside.
+__device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, int W, int H,
+                                          unsigned img, int &inside)
+{
+    const double sx = a.m + b.m + 1e-12 * (1.0 + fabs(a.x) + fabs(b.x));
+    const double sy = a.m + b.m + 1e-12 * (1.0 + fabs(a.y) + fabs(b.y));
+    inside = 0;
+    if ((a.x < -sx && b.x < -sx) || (a.x > W + sx && b.x > W + sx) ||
+        (a.y < -sy && b.y < -sy) || (a.y > H + sy && b.y > H + sy))
+        return true;
+    if (a.code == kFar || b.code == kFar) return false;
+    const int dx = (int)(a.code & 0xffffu) - (int)(b.code & 0xffffu);
+    const int dy = (int)(a.code >> 16) - (int)(b.code >> 16);
+    if (abs(dx) + abs(dy) > 1) return false;
+    inside = (code_in_frame(a.code, W, H) && code_in_frame(b.code, W, H)) ? 1 : 0;
+    if (a.l >= 0) tile_mark(img, a.l);
+    if (b.l >= 0 && b.code != a.code) tile_mark(img, b.l);
+    return true;
+}
+
+// CONTIG: the intervals are contiguous (lo[k+1] == hi[k]); a group is 31
+// intervals, lane j warps the event once at lo of its interval (lane 31 at hi
+// of the last) and takes its segment's far end from lane j + 1.  Otherwise a
+// group is 32 intervals and each lane warps the event at both ends.
+template <bool CONTIG>
 __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
 {
+    constexpr int GS = CONTIG ? 31 : 32;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned int *img = reinterpret_cast<unsigned int *>(smem);
     const int words = a.words;
@@ -569,17 +659,25 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         it.cy = cy;
         it.W = W;
         it.H = H;
-        // lane j evaluates interval g*32 + j
-        const int k = g * 32 + lane;
-        const bool valid = k < a.K;
+        // lane j evaluates interval g*GS + j
+        const int k = g * GS + lane;
+        const bool valid = lane < GS && k < a.K;
         const int kc = valid ? k : a.K - 1;
         it.lo = __ldg(a.lo + kc);
         it.hi = __ldg(a.hi + kc);
         it.dlo = __ldg(a.den_lo + kc);
         it.dhi = __ldg(a.den_hi + kc);
-        const double my_rlo = ddiv(1.0, it.dlo), my_rhi = ddiv(1.0, it.dhi);
-        const double left_hi = __shfl_up_sync(0xffffffffu, it.hi, 1);
-        const bool shared_lo = lane > 0 && it.lo == left_hi;
+        // velocities this lane warps at: CONTIG: lo of its interval, or hi of
+        // the interval before (the group's last point); else lo and hi
+        double nu_a = it.lo, rden_a = ddiv(1.0, it.dlo);
+        double nu_b = it.hi, rden_b = ddiv(1.0, it.dhi);
+        bool has_pt = valid;
+        if (CONTIG && !valid && k <= a.K && lane > 0) {
+            // the point after the last valid interval (its hi)
+            nu_a = __ldg(a.hi + k - 1);
+            rden_a = ddiv(1.0, __ldg(a.den_hi + k - 1));
+            has_pt = true;
+        }
         // Whole-group rejection: the scale s(nu, t) = (1 + nu t) / (1 + nu tau)
         // decreases in nu (ds/dnu = (t - tau) / den^2 <= 0), so every endpoint
         // of the group's segments lies at scale >= s(hmax, t) along the
@@ -587,8 +685,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         // any of them can touch an in-frame pixel (and none is fully inside).
         // Relative errors here are ~1e-15, the slack 1e-9; rounding in the
         // reference's clip is < 1e-3 px while |x'| < 1e12 (kappa).
-        double hmax = valid ? it.hi : -INFINITY, rhmax = my_rhi;
-        double smax = valid ? my_rlo : 0.0;  // s(lo, 0) = 1 / den(lo): the largest scale
+        double hmax = has_pt ? (CONTIG ? nu_a : nu_b) : -INFINITY;
+        double rhmax = CONTIG ? rden_a : rden_b;
+        double smax = has_pt ? rden_a : 0.0;  // s(lo, 0) = 1 / den(lo): the largest scale
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double h2 = __shfl_xor_sync(0xffffffffu, hmax, o);
@@ -597,7 +696,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
             smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
         }
         const double kappa = smax * (hypot(cx, cy) + 1.5) * 1e-12;
-        const TileSink my_sink = it.view.sink(lane);
+        const unsigned my_img = it.view.img + 4u * (unsigned)(lane * words);
         unsigned long long fi = 0;
         int nq = 0, nx = 0;  // queued segments / uncertain pairs (warp-uniform)
         // Events in chunks of 32: lane l loads event l of the chunk (coalesced),
@@ -624,22 +723,21 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
                 const double x = __shfl_sync(0xffffffffu, xl, i);
                 const double y = __shfl_sync(0xffffffffu, yl, i);
                 const double tt = __shfl_sync(0xffffffffu, tl, i);
-                const Warped bq = warp_approx(x, y, tt, it.hi, my_rhi, cx, cy);
-                const double mb = sure_margin(bq, cx, cy);
-                Warped aq;
-                aq.x = __shfl_up_sync(0xffffffffu, bq.x, 1);
-                aq.y = __shfl_up_sync(0xffffffffu, bq.y, 1);
-                double ma = __shfl_up_sync(0xffffffffu, mb, 1);
-                if (!shared_lo) {
-                    aq = warp_approx(x, y, tt, it.lo, my_rlo, cx, cy);
-                    ma = sure_margin(aq, cx, cy);
+                TilePoint pa = tile_point(x, y, tt, nu_a, rden_a, cx, cy, W, H, it.view);
+                TilePoint pb;
+                if (CONTIG) {
+                    pb.x = __shfl_down_sync(0xffffffffu, pa.x, 1);
+                    pb.y = __shfl_down_sync(0xffffffffu, pa.y, 1);
+                    pb.m = __shfl_down_sync(0xffffffffu, pa.m, 1);
+                    pb.code = __shfl_down_sync(0xffffffffu, pa.code, 1);
+                    pb.l = __shfl_down_sync(0xffffffffu, pa.l, 1);
+                } else {
+                    pb = tile_point(x, y, tt, nu_b, rden_b, cx, cy, W, H, it.view);
                 }
                 bool unc = false;
                 if (valid) {
-                    int xa, ya, xb, yb, ins;
-                    if (sure_cells(aq, bq, ma, mb, W, H, xa, ya, xb, yb, ins)) {
-                        if (xa >= 0) my_sink(0, xa, ya);
-                        if (xb >= 0) my_sink(0, xb, yb);
+                    int ins;
+                    if (tile_pair(pa, pb, W, H, my_img, ins)) {
                         if (el < cn.x) fi += ins;
                     } else {
                         unc = true;
@@ -669,7 +767,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         __syncthreads();
         // sum(H), sum(H^2) of each interval's tile image, leaving it zeroed
         const int nw = (m.w + 1) >> 1;
-        for (int j = warp; j < 32; j += kTileWarps) {
+        for (int j = warp; j < GS; j += kTileWarps) {
             unsigned int *im = img + j * words;
             unsigned long long s1 = 0, s2 = 0;
             for (int w = lane; w < nw; w += 32) {
@@ -683,7 +781,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
             }
             s1 = warp_sum(s1);
             s2 = warp_sum(s2);
-            const int kk = g * 32 + j;
+            const int kk = g * GS + j;
             if (lane == 0 && kk < a.K) {
                 if (s1) {
                     atomicAdd(a.marks_s + 2 * kk, s1);
@@ -802,7 +900,7 @@ cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, cons
 }
 
 cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, const double *dlo,
-                       const double *dhi, int K, unsigned long long *fi_out,
+                       const double *dhi, int K, bool contig, unsigned long long *fi_out,
                        unsigned long long *marks_s, int *launches, cudaStream_t s)
 {
     if (f->n_order == 0 || K == 0) return cudaSuccess;
@@ -810,8 +908,9 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = tile_smem_bytes(f->P, f->max_rows);
-    cudaError_t e = cudaFuncSetAttribute(k_frontier_tiles,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = contig ? k_frontier_tiles<true> : k_frontier_tiles<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e) return e;
     TileArgs a;
     a.xs = f->xs;
@@ -824,7 +923,7 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     a.rows = f->rows;
     a.order = f->order;
     a.n_order = f->n_order;
-    a.groups = (K + 31) / 32;
+    a.groups = contig ? (K + 30) / 31 : (K + 31) / 32;
     a.K = K;
     a.lo = lo;
     a.hi = hi;
@@ -841,7 +940,7 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     if ((e = cudaMemsetAsync(f->ctr, 0, sizeof(unsigned int), s))) return e;
     const long long items = (long long)f->n_order * a.groups;
     const int grid = (int)std::min<long long>(sms, items);
-    k_frontier_tiles<<<grid, kTileThreads, smem, s>>>(a);
+    kern<<<grid, kTileThreads, smem, s>>>(a);
     (*launches)++;
     return cudaGetLastError();
 }

@@ -185,10 +185,11 @@ void tiles_free(FrontierTiles *f);
 cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, const double *t,
                       long long n, int W, int H, unsigned long long gen, bool *usable,
                       int *launches, cudaStream_t s);
-// bound_terms for K intervals (every hi <= 0) over the binned window:
+// bound_terms for K intervals (every hi <= 0) over the binned window
+// (contig: lo[k+1] == hi[k] for every k, one warp per endpoint):
 // fi_out[k] += fully_inside, marks_s[2k] += sum(H), marks_s[2k+1] += sum(H^2).
 cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, const double *dlo,
-                       const double *dhi, int K, unsigned long long *fi_out,
+                       const double *dhi, int K, bool contig, unsigned long long *fi_out,
                        unsigned long long *marks_s, int *launches, cudaStream_t s);
 // out[0] tiles (0: frame not tiled), out[1] pixels per tile (max), out[2]
 // listed events of the binned window (-1: not binned / not usable), out[3]
