@@ -14,7 +14,22 @@ step (gamma=0.025, tau=0.5, epsilon=1e-6).
          the result, host wall clock
   --impl reference
          the reference algorithm's CPU implementation (the pinned oracle port,
-         oracle/, every host thread) on the same window and metric
+         oracle/, every host thread) on the same window and metric; the stock
+         numba reference (baseline/_ref/eventdiv, one core) is timed beside it
+         once as cpu_baseline.reference_stock
+
+Extra legs on the same line (each its own workload):
+  solve_cfg3       cfg 3 (640x480, 999,557 events) single-window solve, device
+                   and end to end (the north-star "~1M events in milliseconds")
+  frontier_cfg3    the 4096-leaf frontier in one evd_eval_frontier call (tiled,
+                   images in shared memory), with its own roofline
+  windows_cfg4     2000-window landing sequence: one evd_solve_windows launch
+                   (device), and end to end through
+                   dist.estimate_stream_divergence_dist over the N ranks
+                   (host batches in, every sample gathered on every rank)
+  frontier_cfg5    cfg 5 (1280x720, 5.33 M events): the device-resident exact
+                   solve, and dist.solve_batched_dist (event broadcast + the
+                   batched frontier split over the N ranks)
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 (N>1: launch under torch.distributed.run; ranks solve independent windows.)
@@ -39,7 +54,8 @@ sys.path.insert(0, ROOT)
 
 CONFIG = {"workload": "cfg2: 346x260 window, 204203 events, single-window BnB solve",
           "sensor": "346x260", "events": 204203, "gamma": 0.025, "tau": 0.5,
-          "l2": "flushed between steps (256 MiB write)"}
+          "l2": "flushed between steps (256 MiB write)",
+          "parallelism": "windows: one independent solve per rank (no data-path collective)"}
 METRIC = "divergence solves/sec"
 # cfg 2 runs the speculative-round solve (2 node evaluations per round; the
 # library's policy for windows below 0.5M events on the whole grid)
@@ -148,6 +164,62 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def stock_reference(batch, timeout=600):
+    """One cfg-2 maximise_contrast_bnb of the UNMODIFIED reference package
+    (baseline/_ref/eventdiv: numpy + numba, single-threaded by construction),
+    JIT warmed on a small window first, in a child process (its numba cache in
+    /tmp).  Returns the cpu_baseline.reference_stock record."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "eventdiv")):
+        return {"unavailable": "baseline/_ref/eventdiv not installed"}
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "w.npz")
+        np.savez(path, x=batch.x, y=batch.y, t=batch.t)
+        code = f"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, {ref!r})
+from eventdiv.events import EventBatch, SensorGeometry
+from eventdiv.solver import SolverParams, maximise_contrast_bnb
+z = np.load({path!r})
+g = SensorGeometry({batch.geometry.width}, {batch.geometry.height})
+r = np.random.default_rng(0)
+w = EventBatch(r.uniform(0, 32, 300), r.uniform(0, 32, 300), np.sort(r.uniform(0, 0.5, 300)),
+               0.5, SensorGeometry(32, 32))
+maximise_contrast_bnb(w, SolverParams())   # numba JIT warm-up
+b = EventBatch(z["x"], z["y"], z["t"], {float(batch.tau)!r}, g)
+t0 = time.perf_counter()
+res = maximise_contrast_bnb(b, SolverParams())
+dt = time.perf_counter() - t0
+print(json.dumps({{"s": dt, "nu": res.nu, "contrast": res.contrast, "iterations": res.iterations}}))
+"""
+        env = dict(os.environ, NUMBA_CACHE_DIR=os.path.join(tmp, "numba"),
+                   PYTHONDONTWRITEBYTECODE="1", OMP_NUM_THREADS="1")
+        try:
+            out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                                 timeout=timeout, env=env)
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:
+            return {"unavailable": f"stock reference run failed: {type(e).__name__}"}
+    return {"value": 1.0 / d["s"], "unit": UNIT, "seconds_per_solve": d["s"], "cores": 1,
+            "kind": "reference", "cpu": cpu_model(), "host_cores": host_threads(),
+            "sample": "one full cfg-2 maximise_contrast_bnb of baseline/_ref/eventdiv "
+                      "(numba JIT warmed; single-threaded by construction)",
+            "result": {"nu": d["nu"], "contrast": d["contrast"], "iterations": d["iterations"]}}
+
+
 def run_reference(args, rank, world):
     """The reference algorithm on the host cores (oracle port), rank 0 only."""
     if rank != 0:
@@ -178,19 +250,41 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result": {"nu": r.nu, "contrast": r.contrast, "iterations": r.iterations},
     }
+    if not args.no_stock:
+        line["cpu_baseline"]["reference_stock"] = stock_reference(batch)
     print(json.dumps(line), flush=True)
+
+
+def load_json(*names):
+    """The first of profiles/<name> that exists (newest round first)."""
+    for n in names:
+        f = os.path.join(ROOT, "profiles", n)
+        if os.path.exists(f):
+            with open(f) as fh:
+                return json.load(fh), n
+    return None, None
+
+
+def ncu_val(nc, key):
+    try:
+        return float(str(nc[key][0]).replace(",", ""))
+    except Exception:
+        return None
 
 
 def frontier_line(ctx, stream):
     """Config 3: the 4096-leaf frontier of a 999,557-event 640x480 window in one
-    evd_eval_frontier call (device time, best of 3)."""
+    evd_eval_frontier call (device time, best of 3), tiled path (the 31 images
+    of a work item in shared memory).  Roofline: shared-memory atomics, the
+    marks (= upper_bound_image().in_image_events summed over the leaves) per
+    second against the measured red.shared peak (tools/bench_fp64.cu)."""
     import torch
     from paper_2209_13168_b200 import contrast as con, frontier as fr, synth
     from paper_2209_13168_b200.geometry import velocity_domain
     b = synth.config_window(3)
     lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
     con.load_window(b, ctx)
-    con.frontier_terms(b, lo, hi, ctx=ctx, loaded=True)
+    con.frontier_terms(b, lo, hi, ctx=ctx, loaded=True)  # bins the window (once per window)
     best = None
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -200,9 +294,86 @@ def frontier_line(ctx, stream):
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3
         best = t if best is None else min(best, t)
-    return {"intervals": int(lo.size), "events": int(b.n), "seconds_per_call": best,
-            "events_x_bound_evals_per_s": b.n * lo.size / best,
-            "marks": int(mk.sum()), "atomics_per_s": float(mk.sum()) / best}
+    info = ctx.frontier_info()
+    marks = int(mk.sum())
+    out = {"intervals": int(lo.size), "events": int(b.n), "seconds_per_call": best,
+           "events_x_bound_evals_per_s": b.n * lo.size / best, "marks": marks,
+           "path": {1: "tiles", 2: "global", 3: "global_exact"}.get(info["last_path"]),
+           "tiles": info["tiles"], "listed_events": info["listed_events"]}
+    peaks, _ = load_json("fp64_peak.json")
+    nc, ncf = load_json("ncu_k_frontier_tiles_cfg3_r02.json")
+    if peaks:
+        # Binding roof: the fp64 division pipe.  The algorithm needs
+        # one correctly rounded endpoint warp s = (1 + nu t) / (1 + nu tau) per
+        # event and distinct endpoint -- K + 1 of them for a contiguous frontier
+        # -- i.e. N (K + 1) IEEE quotients per call; achieved = that count per
+        # second against the measured __ddiv_rn throughput.  (The kernel
+        # certifies most of them from a reciprocal product instead of dividing.)
+        pk = peaks.get("ddiv_rn_g_per_s")
+        ach = b.n * (lo.size + 1) / best / 1e9
+        spk = peaks.get("smem_red_u16pair_g_per_s")
+        out["roofline"] = {
+            "bound": "fp64_div", "kernel": "k_frontier_tiles", "achieved": ach, "peak": pk,
+            "unit": "G quotients/s", "frac": ach / pk if pk else None,
+            "traffic": nc.get("dram_bytes") if nc else None, "alg_bytes": 24 * b.n,
+            "note": "achieved = events x (intervals + 1) endpoint warps per call / call time; "
+                    "peak = __ddiv_rn throughput (profiles/fp64_peak.json, tools/bench_fp64.cu); "
+                    "traffic = DRAM bytes of one call (ncu), the images never leave shared memory",
+            "other_roofs": {"smem_atomic": {"achieved": marks / best / 1e9, "peak": spk,
+                                            "unit": "G atomics/s",
+                                            "frac": marks / best / 1e9 / spk if spk else None}}}
+        if nc:
+            out["limiter"] = {
+                "kind": "issue / fp64 latency (certified filtered warps per event x interval)",
+                "issue_active_pct": ncu_val(nc, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_pct": ncu_val(nc, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                "warps_active_pct": ncu_val(nc, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "source": f"profiles/{ncf}"}
+    return out
+
+
+def solve_leg(ctx, stream, flush, cfg, params, steps=5):
+    """One single-window solve of config `cfg` per step: device time with the
+    window resident (L2 flushed before each step), and end to end through
+    maximise_contrast_bnb from pinned host arrays (H2D, solve, D2H)."""
+    import torch
+    import paper_2209_13168_b200 as evd
+    from paper_2209_13168_b200 import solver as sol, synth
+    from paper_2209_13168_b200.contrast import load_window
+    batch = synth.config_window(cfg)
+    load_window(batch, ctx)
+    res, _ = sol.solve_loaded(ctx, params)
+    dev = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res, _ = sol.solve_loaded(ctx, params)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dev.append(e0.elapsed_time(e1) / 1e3)
+    pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(batch, k))).pin_memory()
+           for k in ("x", "y", "t")}
+    pb = evd.EventBatch(pin["x"].numpy(), pin["y"].numpy(), pin["t"].numpy(), batch.tau,
+                        batch.geometry)
+    evd.maximise_contrast_bnb(pb, params)
+    e2e = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = evd.maximise_contrast_bnb(pb, params)
+        e2e.append(time.perf_counter() - t0)
+    return {"events": int(batch.n), "sensor": f"{batch.geometry.width}x{batch.geometry.height}",
+            "device_ms": 1e3 * statistics.median(dev), "device_ms_min": 1e3 * min(dev),
+            "e2e_ms": 1e3 * statistics.median(e2e), "solves_per_s": 1.0 / statistics.median(dev),
+            "e2e_solves_per_s": 1.0 / statistics.median(e2e),
+            "h2d_bytes": 24 * int(batch.n),
+            "result": {"nu": res.nu, "contrast": res.contrast, "bound_gap": res.bound_gap,
+                       "iterations": res.iterations, "bound_evals": res.bound_evals,
+                       "device_rounds": int(res.rounds)},
+            "same_as_public_api": (r.nu, r.contrast, r.iterations) ==
+                                  (res.nu, res.contrast, res.iterations)}
 
 
 def windows_line(ctx):
@@ -215,7 +386,78 @@ def windows_line(ctx):
     res, dev_s, groups = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
     return {"windows": len(batches), "events": int(sum(b.n for b in batches)),
             "device_s": dev_s, "windows_per_s": len(batches) / dev_s, "solver_groups": groups,
-            "all_ok": all(r.status == 0 for r in res)}
+            "all_ok": all(r.status == 0 for r in res)}, batches
+
+
+def barrier_all(world):
+    import torch
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(world, v):
+    import torch
+    if world == 1:
+        return v
+    tt = torch.tensor([v], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def windows_dist_leg(batches, world, reps=3):
+    """Config 4 end to end on N ranks: dist.estimate_stream_divergence_dist over
+    the 2000 host windows -- every rank copies its contiguous shard (balanced
+    by events) to its GPU, solves it in one launch and the per-window samples
+    are all-gathered; wall time between barriers, max over ranks (fixed total
+    work: strong scaling)."""
+    import paper_2209_13168_b200 as evd
+    from paper_2209_13168_b200 import dist as pdist
+    params = evd.SolverParams()
+    out = pdist.estimate_stream_divergence_dist(batches, params)  # warm-up
+    best = None
+    for _ in range(reps):
+        barrier_all(world)
+        t0 = time.perf_counter()
+        out = pdist.estimate_stream_divergence_dist(batches, params)
+        barrier_all(world)
+        t = max_over_ranks(world, time.perf_counter() - t0)
+        best = t if best is None else min(best, t)
+    return {"windows": len(batches), "ranks": world, "e2e_s": best,
+            "windows_per_s": len(batches) / best, "samples": len(out),
+            "h2d_bytes": 24 * int(sum(b.n for b in batches)),
+            "scaling": "strong (2000 windows split over the ranks)"}
+
+
+def cfg5_leg(world, rank):
+    """Config 5 (1280x720, 5,327,641 events): the single-GPU device-resident
+    exact solve (maximise_contrast_bnb) and dist.solve_batched_dist on the N
+    ranks (events broadcast once over NCCL, each round's evaluations split
+    over the ranks, results all-gathered; certified within gamma)."""
+    import torch
+    import paper_2209_13168_b200 as evd
+    from paper_2209_13168_b200 import dist as pdist, synth
+    params = evd.SolverParams()
+    batch = synth.config_window(5) if rank == 0 else None
+    out = {"events": 5327641, "sensor": "1280x720", "ranks": world}
+    if rank == 0:
+        evd.maximise_contrast_bnb(batch, params)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = evd.maximise_contrast_bnb(batch, params)
+        out["exact_solve_e2e_s"] = time.perf_counter() - t0
+        out["exact"] = {"nu": r.nu, "contrast": r.contrast, "iterations": r.iterations}
+    pdist.solve_batched_dist(batch, params, k=64)  # warm-up (broadcast + evaluators)
+    barrier_all(world)
+    t0 = time.perf_counter()
+    rb = pdist.solve_batched_dist(batch, params, k=64)
+    barrier_all(world)
+    out["batched_dist_e2e_s"] = max_over_ranks(world, time.perf_counter() - t0)
+    out["batched"] = {"nu": rb.nu, "contrast": rb.contrast, "rounds": rb.rounds,
+                      "nodes": rb.nodes, "bound_evals": rb.bound_evals, "k": 64}
+    if rank == 0:
+        out["batched_within_gamma"] = rb.contrast >= out["exact"]["contrast"] - params.gamma
+    return out
 
 
 def stream_line():
@@ -238,8 +480,18 @@ def run_gpu(args, rank, world, local):
 
     torch.cuda.set_device(local)
     _lib.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if world == 1 and not args.no_extra:
+        # a one-rank NCCL group, so the multi-GPU legs run their real code path
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local))
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     batch = synth.config_window(2)
     params = evd.SolverParams()
@@ -305,6 +557,22 @@ def run_gpu(args, rank, world, local):
         t_e2e = float(tt.item())
     e2e = world * args.steps / t_e2e
 
+    # ---------------- extra legs (all ranks take part in the multi-rank ones)
+    extra = {}
+    if not args.no_extra:
+        if world == 1:
+            extra["frontier_cfg3"] = frontier_line(ctx, stream)
+            extra["solve_cfg3"] = solve_leg(ctx, stream, flush, 3, params)
+            wl, batches = windows_line(ctx)
+            extra["windows_cfg4"] = wl
+        else:
+            from paper_2209_13168_b200 import synth as _s
+            batches = [_s.sequence_window(k) for k in range(2000)]
+        extra["windows_cfg4_dist"] = windows_dist_leg(batches, world)
+        extra["frontier_cfg5"] = cfg5_leg(world, rank)
+        if world == 1:
+            extra["stream_e2e"] = stream_line()
+
     if rank == 0:
         peaks = {}
         try:
@@ -313,84 +581,87 @@ def run_gpu(args, rank, world, local):
         except Exception:
             pass
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        # algorithmic bytes of k_solve: each node evaluation streams the window
-        # once (24 B/event: x, y, t); images are not algorithmic
-        alg_bytes = 24.0 * batch.n * res.point_evals
         k_ms = statistics.mean(kernel_ms)
-        achieved = alg_bytes / (k_ms / 1e3) / 1e9
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tfile):
-            with open(tfile) as fh:
-                traffic = json.load(fh).get("k_solve_dram_bytes")
-        # atomic roofline: every pixel increment is one L2 RED; peak measured by
-        # tools/bench_atomics.cu for this image size (profiles/atomic_peak.json)
-        atomic = None
-        afile = os.path.join(ROOT, "profiles", "atomic_peak.json")
-        if os.path.exists(afile):
-            with open(afile) as fh:
-                apk = json.load(fh).get("random_m89960_gatomics_per_s")
-            ach = res.marks / (k_ms / 1e3) / 1e9
-            atomic = {"achieved": ach, "peak": apk, "unit": "G atomics/s",
-                      "frac": ach / apk if apk else None, "marks_per_solve": int(res.marks),
-                      "peak_source": "tools/bench_atomics.cu (u32 RED, random pixels, M=89960)"}
-        # what does bound the kernel: issue and occupancy from the committed
-        # ncu --set full capture of this launch (profiles/, tools/round_evidence.sh)
+        # Node evaluations the kernel actually executed, speculative slots
+        # included: every evaluation passes over all n events (exact_events)
+        node_evals = int(round(res.exact_events / batch.n))
+        nc, ncf = load_json("ncu_k_solve_cfg2_r02.json", "ncu_k_solve_cfg2_r01.json")
+        traffic = nc.get("dram_bytes") if nc and "dram_bytes" in nc else None
+        if nc and traffic is None:
+            tb = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            traffic = int(sum(ncu_val(nc, k) * tb.get(nc[k][1], 1)
+                              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
+        # binding roof of k_solve_spec: every pixel increment is one L2 RED
+        # (explicit red.global), marks = the reference's in_image_events summed
+        # over the solve's images; peak measured by tools/bench_atomics.cu at
+        # this image size (profiles/atomic_peak.json).  HBM is not binding: the
+        # window is L2-resident, DRAM traffic is below the algorithmic bytes.
+        apk_all, _ = load_json("atomic_peak.json")
+        apk = (apk_all or {}).get("random_m89960_gatomics_per_s")
+        ach = res.marks / (k_ms / 1e3) / 1e9
+        alg_bytes = 24.0 * batch.n * node_evals
+        hbm_ach = alg_bytes / (k_ms / 1e3) / 1e9
+        fp64pk, _ = load_json("fp64_peak.json")
         limiter = None
-        nfile = os.path.join(ROOT, "profiles", "ncu_k_solve_cfg2_r01.json")
-        if os.path.exists(nfile):
-            with open(nfile) as fh:
-                nc = json.load(fh)
-            g = lambda k: float(nc[k][0]) if k in nc else None
+        if nc:
             limiter = {
                 "kind": "latency / issue (sequential BnB rounds; per-warp dependent chains)",
-                "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
-                "fp64_pipe_pct": g("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-                "threads_per_warp_inst": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
-                "registers_per_thread": g("launch__registers_per_thread"),
-                "source": "profiles/ncu_k_solve_cfg2_r01.json"}
+                "issue_active_pct": ncu_val(nc, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "warps_active_pct": ncu_val(nc, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_pct": ncu_val(nc, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                "threads_per_warp_inst": ncu_val(nc, "smsp__thread_inst_executed_per_inst_executed.ratio"),
+                "registers_per_thread": ncu_val(nc, "launch__registers_per_thread"),
+                "source": f"profiles/{ncf}"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference simulator restated, bit-identical window)",
-            "config": dict(CONFIG, parallelism=f"windows x{world} (no data-path collective)"),
+            "config": CONFIG,
             "events_x_bound_evals_per_s": world * batch.n * res.bound_evals * args.steps / t_dev,
             "solve": {"nu": res.nu, "contrast": res.contrast, "bound_gap": res.bound_gap,
                       "iterations": res.iterations, "bound_evals": res.bound_evals,
-                      "point_evals": res.point_evals, "max_frontier": res.max_frontier,
-                      "marks": int(res.marks), "kernel_ms": k_ms,
-                      "device_rounds": int(res.rounds)},
-            "atomic_roofline": atomic,
-            "limiter": limiter,
+                      "point_evals": res.point_evals, "node_evals": node_evals,
+                      "max_frontier": res.max_frontier, "marks": int(res.marks),
+                      "kernel_ms": k_ms, "device_rounds": int(res.rounds)},
             # per step: x, y, t (f64) and the window offsets in; one WindowResult
             # (evd_internal.h) out
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 24 * batch.n + 16,
                     "d2h_bytes_per_step": ctypes.sizeof(_lib.WindowResult)},
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "roofline": {"bound": "hbm", "kernel": KERNEL, "achieved": achieved,
-                         "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic,
-                         "note": "latency-bound sequential BnB: grid-wide rounds of node "
-                                 "evaluations; algorithmic bytes = 24 B x events x node evals"},
+            "roofline": {"bound": "atomic", "kernel": KERNEL, "achieved": ach, "peak": apk,
+                         "unit": "G atomics/s", "frac": ach / apk if apk else None,
+                         "traffic": traffic, "marks_per_launch": int(res.marks),
+                         "note": "achieved = marks per solve (sum of every image's "
+                                 "in_image_events) / mean kernel time; peak = u32 RED at "
+                                 "M=89,960 (tools/bench_atomics.cu); traffic = DRAM bytes of "
+                                 "one launch (ncu --set full)",
+                         "other_roofs": {
+                             "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
+                                     "frac": hbm_ach / hbm_peak,
+                                     "alg_bytes": alg_bytes,
+                                     "note": "24 B x events x node evaluations; the window is "
+                                             "L2-resident"},
+                             "fp64_pipe_pct": limiter["fp64_pipe_pct"] if limiter else None,
+                             "fp64_peaks": fp64pk}},
+            "limiter": limiter,
         }
-        if world == 1 and not args.no_extra:
-            line["frontier_cfg3"] = frontier_line(ctx, stream)
-            line["windows_cfg4"] = windows_line(ctx)
-            line["stream_e2e"] = stream_line()
+        line.update(extra)
         if world == 1 and not args.no_cpu:
             threads = host_threads()
             dt, r = cpu_solve_sample(batch, threads)
             same = (r.nu, r.contrast, r.iterations) == (res.nu, res.contrast, res.iterations)
             line["cpu_baseline"] = {
                 "value": 1.0 / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                "cpu": cpu_model(),
                 "sample": "one full cfg-2 BnB solve (oracle/ C restatement of the reference, "
                           f"events split over {threads} threads); identical result: {same}"}
+            if not args.no_stock:
+                line["cpu_baseline"]["reference_stock"] = stock_reference(batch)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def main():
@@ -401,7 +672,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-extra", action="store_true",
-                    help="skip the config-3 frontier and config-4 window lines")
+                    help="skip the config-3/4/5 legs")
+    ap.add_argument("--no-stock", action="store_true",
+                    help="skip timing the stock numba reference (baseline/_ref)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
