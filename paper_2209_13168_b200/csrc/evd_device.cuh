@@ -11,10 +11,25 @@
 //   fully-inside    pkg/src/eventdiv/contrast.py:195-201
 //   pairwise sum    numpy float64 pairwise summation behind np.sum (contrast.py:64)
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace evd {
+
+// Device-side bounds checks, compiled into libevd_checked.so only
+// (-DEVD_CHECKED; tests/test_gpu_checked.py runs the GPU suite on it): every
+// mark lands inside the frame with p == y * W + x, queue slots stay inside
+// their arrays.  A failed check traps the kernel (cudaErrorAssert).
+#ifdef EVD_CHECKED
+#define EVD_CHECK(cond) assert(cond)
+#else
+#define EVD_CHECK(cond) ((void)0)
+#endif
+__device__ __forceinline__ void check_mark(long long p, int x, int y, int W, int H)
+{
+    EVD_CHECK(x >= 0 && x < W && y >= 0 && y < H && p == (long long)y * W + x);
+}
 
 // ---------------------------------------------------------------- exact fp64
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -187,10 +202,10 @@ __device__ __forceinline__ int mark_point(double px, double py, int W, int H, Pr
     const bool fy0 = (unsigned)r.y0 < (unsigned)H, fy1 = sy && (unsigned)r.y1 < (unsigned)H;
     const int base = r.y0 * W + r.x0;  // the frame has < 2^31 pixels
     int marks = 0;
-    if (fx0 && fy0 && !(px0 && py0)) { sink(base, r.x0, r.y0); marks++; }
-    if (fx1 && fy0 && !(px1 && py0)) { sink(base + 1, r.x1, r.y0); marks++; }
-    if (fx0 && fy1 && !(px0 && py1)) { sink(base + W, r.x0, r.y1); marks++; }
-    if (fx1 && fy1 && !(px1 && py1)) { sink(base + W + 1, r.x1, r.y1); marks++; }
+    if (fx0 && fy0 && !(px0 && py0)) { check_mark(base, r.x0, r.y0, W, H); sink(base, r.x0, r.y0); marks++; }
+    if (fx1 && fy0 && !(px1 && py0)) { check_mark(base + 1, r.x1, r.y0, W, H); sink(base + 1, r.x1, r.y0); marks++; }
+    if (fx0 && fy1 && !(px0 && py1)) { check_mark(base + W, r.x0, r.y1, W, H); sink(base + W, r.x0, r.y1); marks++; }
+    if (fx1 && fy1 && !(px1 && py1)) { check_mark(base + W + 1, r.x1, r.y1, W, H); sink(base + W + 1, r.x1, r.y1); marks++; }
     prev = r;
     return marks;
 }
@@ -208,6 +223,7 @@ __device__ __forceinline__ int mark_interior(double px, double py, int W, int H,
         const bool seen = ix >= prev.x0 && ix <= prev.x1 && iy >= prev.y0 && iy <= prev.y1;
         prev = Prev{ix, ix, iy, iy};
         if (!seen && (unsigned)ix < (unsigned)W && (unsigned)iy < (unsigned)H) {
+            check_mark(iy * W + ix, ix, iy, W, H);
             sink(iy * W + ix, ix, iy);
             return 1;
         }
@@ -302,7 +318,11 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
 {
     if (ax == bx && ay == by) {  // degenerate: floor rule, not the closed-square rule
         const long long p = floor_bin(ax, ay, W, H);
-        if (p >= 0) { sink(p, (int)(p % W), (int)(p / W)); marks++; }
+        if (p >= 0) {
+            check_mark(p, (int)(p % W), (int)(p / W), W, H);
+            sink(p, (int)(p % W), (int)(p / W));
+            marks++;
+        }
         return 0;
     }
     // Division-free rejection, exact: every sample the reference would mark
@@ -359,10 +379,12 @@ __device__ __forceinline__ int build_segment(double ax, double ay, double bx, do
         if (fx0 != x0 && fy0 != y0 && fx1 != x1 && fy1 != y1 &&
             fabs(fx1 - fx0) + fabs(fy1 - fy0) <= 1.0) {
             if (fx0 >= 0.0 && fx0 < W && fy0 >= 0.0 && fy0 < H) {
+                check_mark((long long)fy0 * W + (long long)fx0, (int)fx0, (int)fy0, W, H);
                 sink((long long)fy0 * W + (long long)fx0, (int)fx0, (int)fy0);
                 marks++;
             }
             if ((fx1 != fx0 || fy1 != fy0) && fx1 >= 0.0 && fx1 < W && fy1 >= 0.0 && fy1 < H) {
+                check_mark((long long)fy1 * W + (long long)fx1, (int)fx1, (int)fy1, W, H);
                 sink((long long)fy1 * W + (long long)fx1, (int)fx1, (int)fy1);
                 marks++;
             }

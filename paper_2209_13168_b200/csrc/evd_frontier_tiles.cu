@@ -52,6 +52,7 @@ constexpr double kTileDelta = 0.75;  // > sqrt(2)/2 + rounding of the sampled po
 constexpr int kTileThreads = 512;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kTileMaxEvents = 65535;  // u16 counters
+constexpr int kTileMaxWords = 32768;   // bound on a tile image's words (checked builds)
 
 // ---------------------------------------------------------------- host plan
 namespace {
@@ -372,6 +373,7 @@ struct TileSink {
             int l = -1;
             if (x >= xl && x <= xh) l = e1 + x - xl;
             else if (x >= xl2 && x <= xh2) l = e3 + x - xl2;
+            EVD_CHECK(l < 2 * kTileMaxWords);
             if (l >= 0)
                 asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(img + 4u * (unsigned)(l >> 1)),
                              "r"(1u << ((l & 1) << 4))
@@ -518,6 +520,7 @@ __device__ __noinline__ int tile_exact(TileQueue &q, int nx, int take, int nq,
     const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
     if (c > 0) {
         const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+        EVD_CHECK(slot < 64);
         q.d[slot] = d;
         q.jj[slot] = (unsigned char)j;
     }
@@ -558,6 +561,7 @@ __device__ __forceinline__ int tile_local(const TileView &v, int x, int y)
 
 __device__ __forceinline__ void tile_mark(unsigned img, int l)
 {
+    EVD_CHECK(l >= 0 && l < 2 * kTileMaxWords);
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(img + 4u * (unsigned)(l >> 1)),
                  "r"(1u << ((l & 1) << 4))
                  : "memory");

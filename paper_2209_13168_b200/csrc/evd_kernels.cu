@@ -107,6 +107,7 @@ __device__ __forceinline__ int segment_or_queue_inl(double ax, double ay, double
     SegDesc d;
     const int c = build_segment(ax, ay, bx, by, W, H, C, d, sink, marks);
     if (c == 0) return 0;
+    EVD_CHECK(slot >= 0 && slot < 64);
     q.d[slot] = d;
     q.img[slot] = sink.img;
     return c;
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier(
         const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
         if (c > 0) {
             const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+            EVD_CHECK(slot < 64);
             wq.d[slot] = d;
             wq.img[slot] = img;
         }
@@ -444,6 +446,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier_f(
         const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
         if (c > 0) {
             const int slot = nq + __popc(bal & ((1u << lane) - 1u));
+            EVD_CHECK(slot < 64);
             wq.d[slot] = d;
             wq.img[slot] = sj.img;
         }
@@ -472,6 +475,7 @@ __global__ void __launch_bounds__(kThreads) k_frontier_f(
             long long pix, pix2;
             int ins;
             if (sure_segment_adj(aq, bq, ma, mb, W, H, pix, pix2, ins)) {
+                EVD_CHECK(pix < M && pix2 < M);
                 if (pix >= 0) sink(pix, 0, 0);
                 if (pix2 >= 0) sink(pix2, 0, 0);
                 fi += ins;
