@@ -332,6 +332,20 @@ def frontier_line(ctx, stream):
     return out
 
 
+def ref_loop_leg():
+    """The reference's own BnB loop (baseline/_ref solver.py, Python heapq)
+    with contrast_at / bound_terms bound to the drop-in,
+    cfg 2, resident-window cache on and off (tools/ref_loop_bench.py)."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "eventdiv")):
+        return {"unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_loop_bench.py"), "2"],
+                         capture_output=True, text=True, timeout=600)
+    try:
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return {"error": (out.stderr or out.stdout)[-300:]}
+
+
 def solve_leg(ctx, stream, flush, cfg, params, steps=5):
     """One single-window solve of config `cfg` per step: device time with the
     window resident (L2 flushed before each step), and end to end through
@@ -572,6 +586,7 @@ def run_gpu(args, rank, world, local):
         extra["frontier_cfg5"] = cfg5_leg(world, rank)
         if world == 1:
             extra["stream_e2e"] = stream_line()
+            extra["reference_loop_drop_in"] = ref_loop_leg()
 
     if rank == 0:
         peaks = {}

@@ -51,6 +51,11 @@ const char *evd_last_error(const evd_ctx *ctx);
 int evd_set_stream(evd_ctx *ctx, void *cuda_stream);
 /* Number of kernels this context has launched so far. */
 int64_t evd_kernel_launches(const evd_ctx *ctx);
+/* Generation of the resident window: changes whenever a call replaces it
+ * (evd_set_events, the stream solves).  A binding that keeps one window
+ * resident across per-call entry points (bound_terms, contrast_at, ...)
+ * re-uploads only when the generation or the caller's arrays changed. */
+int64_t evd_window_generation(const evd_ctx *ctx);
 /* SM count of the context's device. */
 int evd_device_sms(const evd_ctx *ctx);
 

@@ -25,6 +25,7 @@ FRONTIER_AUTO, FRONTIER_TILES, FRONTIER_GLOBAL, FRONTIER_GLOBAL_EXACT = 0, 1, 2,
 # every symbol include/evd.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
     "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
+    "evd_window_generation",
     "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_set_option",
     "evd_frontier_info", "evd_image_contrast",
@@ -88,6 +89,7 @@ _SIGS = {
     "evd_last_error": (ctypes.c_char_p, [_vp]),
     "evd_set_stream": (ctypes.c_int, [_vp, _vp]),
     "evd_kernel_launches": (_i64, [_vp]),
+    "evd_window_generation": (_i64, [_vp]),
     "evd_device_sms": (ctypes.c_int, [_vp]),
     "evd_set_events": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64]),
     "evd_radial_warp": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _f64, _f64, _i32, _i32, _d, _d]),
@@ -156,6 +158,8 @@ def set_device(device: int) -> None:
 class Context:
     """One libevd context (device buffers, stream) for the calling thread."""
 
+    _resident = None  # contrast.load_window's record of the resident window
+
     def __init__(self, device: int):
         self.lib = load()
         h = _vp()
@@ -176,6 +180,10 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    @property
+    def window_generation(self) -> int:
+        return int(self.lib.evd_window_generation(self.h))
 
     def error_text(self) -> str:
         return self.lib.evd_last_error(self.h).decode()

@@ -54,15 +54,47 @@ def _raise(ctx, rc):
     raise _lib.EvdError(rc, ctx.error_text())
 
 
+WINDOW_CACHE = True  # keep one window resident across per-call entry points
+
+
+def _same_window(ctx, key, arrays) -> bool:
+    """The window resident in ctx is exactly these arrays' current contents:
+    same arrays, frame and tau, the context's window untouched since
+    (evd_window_generation), and -- unless all three arrays are read-only --
+    bit-identical contents to the host copy taken at upload (exact compare of
+    the uint64 views, ~0.6 ms at 200 k events, against a ~1.5 ms re-upload)."""
+    res = getattr(ctx, "_resident", None)
+    if not WINDOW_CACHE or res is None or res[0] != key or res[1] != ctx.window_generation:
+        return False
+    if all(not a.flags.writeable for a in arrays):
+        return all(a is c for a, c in zip(arrays, res[2]))
+    return all(np.array_equal(a.view(np.uint64), c.view(np.uint64))
+               for a, c in zip(arrays, res[2]))
+
+
 def load_window(batch: EventBatch, ctx=None):
-    """Copy a window's events to the device (evd_set_events); returns the context."""
+    """Make the window resident on the device (evd_set_events); returns the
+    context.  The per-call entry points (accumulate_image, contrast_at,
+    upper_bound_image, bound_terms, ...) call it every time, as the reference
+    recomputes from the batch every time; a window already resident with
+    identical contents is not uploaded again (_same_window)."""
     ctx = ctx or _lib.context()
     g = batch.geometry
     x, y, t = _lib.f64(batch.x), _lib.f64(batch.y), _lib.f64(batch.t)
+    key = (x.ctypes.data, y.ctypes.data, t.ctypes.data, t.size, g.width, g.height,
+           float(batch.tau))
+    if _same_window(ctx, key, (x, y, t)):
+        return ctx
+    ctx._resident = None
     rc = ctx.lib.evd_set_events(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t), t.size,
                                 g.width, g.height, float(batch.tau))
     if rc:
         _raise(ctx, rc)
+    # read-only arrays: held (so their buffers cannot be freed and reused at
+    # the same address); writeable ones: a copy to compare against
+    frozen = all(not a.flags.writeable for a in (x, y, t))
+    ctx._resident = (key, ctx.window_generation,
+                     (x, y, t) if frozen else (x.copy(), y.copy(), t.copy()))
     return ctx
 
 

@@ -504,6 +504,8 @@ int evd_set_stream(evd_ctx *ctx, void *cuda_stream)
 
 int64_t evd_kernel_launches(const evd_ctx *ctx) { return ctx ? ctx->launches : -1; }
 
+int64_t evd_window_generation(const evd_ctx *ctx) { return ctx ? (int64_t)ctx->gen : -1; }
+
 int evd_device_sms(const evd_ctx *ctx) { return ctx ? ctx->sms : -1; }
 
 int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
