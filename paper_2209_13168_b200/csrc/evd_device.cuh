@@ -507,6 +507,14 @@ __device__ __forceinline__ bool cursor_init(const SegDesc &d, int j, Cursor &c)
 // One item: mark it, find its successor (the list it comes from shifts its
 // lookahead and refills it with one division on selected operands, so lanes
 // stay converged), mark the midpoint.  Returns false once the chunk is done.
+//
+// The segment's end samples ts = 0 and ts = 1 (closed-square calls, the
+// costliest marks) are not marked here but by cursor_head / cursor_tail,
+// once per chunk outside the step loop: inside it a warp paid for them on
+// ~60% of its steps (some lane is almost always at an end sample), outside
+// it pays once per round.  The calls happen in the same order with the same
+// dedup state, so the marks are unchanged.  c.fin on return: the chunk ends
+// with the trailing sample, still to be marked by cursor_tail.
 #ifdef EVD_OUTLINE_STEP
 #define EVD_STEP_INLINE __noinline__
 #else
@@ -520,18 +528,14 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
     // A grid-line crossing whose other coordinate is not near a grid line
     // marks only pixels of the cells of the midpoints on either side of it,
     // which mark them anyway (plain_crossing), so its call adds no pixel and
-    // is skipped; the leading / trailing samples and near-corner crossings
-    // take the reference's closed-square call.
-    if (EVD_SKIP_PLAIN && c.kind != 0) {
+    // is skipped; near-corner crossings take the reference's closed-square
+    // call.  (kind 0: the leading sample, already marked by cursor_head.)
+    if (c.kind != 0) {
         const double o = c.kind == 1 ? dadd(cy0, dmul(c.cur, ddy)) : dadd(cx0, dmul(c.cur, ddx));
-        if (!plain_crossing(o))
+        if (!(EVD_SKIP_PLAIN && plain_crossing(o)))
             marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H,
                                 c.prev, sink);
-    } else {
-        marks += mark_point(dadd(cx0, dmul(c.cur, ddx)), dadd(cy0, dmul(c.cur, ddy)), W, H,
-                            c.prev, sink);
     }
-    if (c.fin) return false;  // the trailing ts = 1 has no successor
     const bool tX = c.sX < 2.0 && c.sX <= c.sY;
     const bool tY = !tX && c.sY < 2.0;
     double nxt = 1.0;  // the trailing ts = 1 when both lists are spent
@@ -556,13 +560,40 @@ __device__ EVD_STEP_INLINE bool cursor_step(const SegDesc &d, Cursor &c, int W, 
             c.kY = dadd(c.kY, (double)d.Y.step);
         }
     } else {
-        c.fin = 1;
         c.kind = 0;
     }
     const double sm = dmul(0.5, dadd(c.cur, nxt));
     marks += mark_interior(dadd(cx0, dmul(sm, ddx)), dadd(cy0, dmul(sm, ddy)), W, H, c.prev, sink);
     c.cur = nxt;
-    return --c.left > 0;
+    if (--c.left == 0) return false;  // the next item (trailing or not) starts the next chunk
+    c.fin = (tX || tY) ? 0 : 1;       // the trailing sample is this chunk's last item
+    return !c.fin;
+}
+
+// Before a chunk's steps: the leading sample ts = 0 of a segment's first chunk
+// (the reference's closed-square call).  Returns whether the chunk has steps
+// (a chunk holding only the trailing sample has none: c.fin).
+template <class Sink>
+__device__ __forceinline__ bool cursor_head(const SegDesc &d, Cursor &c, int W, int H, Sink &sink,
+                                            int &marks)
+{
+    if (c.fin) return false;
+    if (c.kind == 0)
+        marks += mark_point(dadd(d.X.c0, dmul(0.0, d.X.dd)), dadd(d.Y.c0, dmul(0.0, d.Y.dd)), W,
+                            H, c.prev, sink);  // p(0), the reference's expression
+    return true;
+}
+
+// After a chunk's steps: the trailing sample ts = 1 when it is in this chunk.
+template <class Sink>
+__device__ __forceinline__ void cursor_tail(const SegDesc &d, const Cursor &c, int W, int H,
+                                            Sink &sink, int &marks)
+{
+    if (c.fin) {
+        Prev prev = c.prev;
+        marks += mark_point(dadd(d.X.c0, dmul(1.0, d.X.dd)), dadd(d.Y.c0, dmul(1.0, d.Y.dd)), W, H,
+                            prev, sink);
+    }
 }
 
 // Sample chunk j of a built segment to the end.
@@ -571,9 +602,12 @@ __device__ __forceinline__ int sample_chunk(const SegDesc &d, int j, int W, int 
 {
     Cursor c;
     int marks = 0;
-    if (cursor_init(d, j, c))
-        while (cursor_step(d, c, W, H, sink, marks)) {
-        }
+    if (cursor_init(d, j, c)) {
+        if (cursor_head(d, c, W, H, sink, marks))
+            while (cursor_step(d, c, W, H, sink, marks)) {
+            }
+        cursor_tail(d, c, W, H, sink, marks);
+    }
     return marks;
 }
 

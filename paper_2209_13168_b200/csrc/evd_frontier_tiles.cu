@@ -429,8 +429,11 @@ __device__ __noinline__ void tile_drain(TileQueue &q, int nq, int W, int H, Tile
         }
         const SegDesc d = q.d[slot];
         TileSink sink = v.sink(q.jj[slot]);
+        const bool live = active;
+        if (active) active = cursor_head(d, c, W, H, sink, marks);
         while (__any_sync(0xffffffffu, active))
             if (active) active = cursor_step(d, c, W, H, sink, marks);
+        if (live) cursor_tail(d, c, W, H, sink, marks);
     }
     __syncwarp();
 }

@@ -173,8 +173,11 @@ __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int 
             active = cursor_init(q.d[slot], second ? r - q.na[L] : r, c);
         }
         const SegDesc d = q.d[slot];  // in registers for the walk
+        const bool live = active;
+        if (active) active = cursor_head(d, c, W, H, sink, marks);
         while (__any_sync(0xffffffffu, active))
             if (active) active = cursor_step(d, c, W, H, sink, marks);
+        if (live) cursor_tail(d, c, W, H, sink, marks);
     }
     __syncwarp();
     return marks;
@@ -219,8 +222,11 @@ __device__ __noinline__ int warp_drain_list(WarpQueue &q, int nq, int W, int H)
             active = cursor_init(q.d[slot], t - q.off[L], c);
         }
         const SegDesc d = q.d[slot];
+        const bool live = active;
+        if (active) active = cursor_head(d, c, W, H, sink, marks);
         while (__any_sync(0xffffffffu, active))
             if (active) active = cursor_step(d, c, W, H, sink, marks);
+        if (live) cursor_tail(d, c, W, H, sink, marks);
     }
     __syncwarp();
     return marks;
