@@ -101,6 +101,8 @@ struct FrontierTiles {
     size_t xs_cap = 0, ys_cap = 0, ts_cap = 0;
     float *rho = nullptr;           // per listed event: frame-exit scale (see k_tile_fill)
     size_t rho_cap = 0;
+    float2 *xyf = nullptr;          // per listed event: RN32 of the centred coordinates
+    size_t xyf_cap = 0;
     int *order = nullptr;           // tiles with work, heaviest list first
     size_t order_cap = 0;
     int n_order = 0;
@@ -116,7 +118,7 @@ void tiles_free(FrontierTiles *f)
     if (!f) return;
     for (void *p : {(void *)f->meta, (void *)f->rows, (void *)f->ang, (void *)f->start,
                     (void *)f->cnt, (void *)f->cursor, (void *)f->flag, (void *)f->xs,
-                    (void *)f->ys, (void *)f->ts, (void *)f->rho, (void *)f->order,
+                    (void *)f->ys, (void *)f->ts, (void *)f->rho, (void *)f->xyf, (void *)f->order,
                     (void *)f->ctr})
         if (p) cudaFree(p);
     delete f;
@@ -315,7 +317,10 @@ __global__ void k_tile_count(const double *__restrict__ xc, const double *__rest
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double x = xc[i], y = yc[i], tt = t[i];
-        if (!isfinite(x) || !isfinite(y) || !isfinite(tt)) {
+        // the tiled path takes finite events within 1e5 px of the FOE (its
+        // certified fp32 positions then stay below 1e11 px at any scale up to
+        // 1e6, see tile_point); the rest of the windows take the global path
+        if (!isfinite(tt) || !(fabs(x) <= 1e5) || !(fabs(y) <= 1e5)) {
             *flag = 1u;
             continue;
         }
@@ -334,7 +339,7 @@ __global__ void k_tile_count(const double *__restrict__ xc, const double *__rest
 __global__ void k_tile_fill(const double *__restrict__ xc, const double *__restrict__ yc,
                             const double *__restrict__ t, long long n, TileGeom g, double cx,
                             double cy, unsigned long long *cursor, double *xs, double *ys,
-                            double *ts, float *rho)
+                            double *ts, float *rho, float2 *xyf)
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -348,6 +353,7 @@ __global__ void k_tile_fill(const double *__restrict__ xc, const double *__restr
             ys[p] = y;
             ts[p] = tt;
             rho[p] = q;
+            xyf[p] = make_float2(__double2float_rn(x), __double2float_rn(y));
         });
     }
 }
@@ -468,6 +474,7 @@ __device__ __forceinline__ bool sure_cells(const Warped &a, const Warped &b, dou
 struct TileArgs {
     const double *xs, *ys, *ts;  // listed events, tile-major
     const float *rho;            // their frame-exit scales
+    const float2 *xyf;           // their centred coordinates rounded to float
     const long long *start;
     const int2 *cnt;             // (home, all)
     const int4 *meta;
@@ -541,84 +548,115 @@ __device__ __noinline__ int tile_exact(TileQueue &q, int nx, int take, int nq,
 // code = (fy + 2) << 16 | (fx + 2) when the exact position lies surely
 // strictly inside cell (fx, fy) with -2 <= fx, fy <= 32000, else kFar.
 constexpr unsigned kFar = 0xffffffffu;
+
+// One endpoint of the filtered path in fp32.  The scale s = (1 + nu t) *
+// RN(1 / den) is formed in binary64 (within 4.4e-16 |s| of the reference's
+// RN((1 + nu t) / den): three roundings each), then the position in fp32,
+// shifted by +8 px so every cell a certified point can touch has a positive
+// index: X = RN32(RN32(xc) * RN32(s) + (cx + 8)), one FMA.  Against the
+// reference's binary64 x' = RN(cx + RN(xc * s)):
+//   |X - 8 - x'| <= |xc s| (2^-24 + 2^-24 + 2^-48 + 4.4e-16)   (RN32 of xc, s)
+//                 + 2^-24 |X|                                  (the FMA)
+//                 + 2^-53 (|xc s| + |x'|)                      (the reference)
+//               <= 1.81e-7 |X| + 1.2e-7 (cx + 8) + 1e-12       (|xc s| <= |X| + cx + 8)
+// so m = 1.9e-7 |X| + K, K = 1.25e-7 (c + 8) + 1e-9 (one fmaf; its own
+// rounding is inside the 1.9 / 1.81 slack) bounds the error.  A coordinate is
+// certified strictly inside its cell when 1 <= X <= 32000 and its fraction
+// f = X - floor(X) (exact: Sterbenz) has f > m and f < 1 - 2m (RN32(1 - 2m)
+// errs by <= 2^-25 < m since m >= 1.9e-7).
 struct TilePoint {
-    double x, y, m;
-    unsigned code;
-    int l;
+    float x, y, m;   // shifted position (+8) and its error bound
+    unsigned code;   // (iy + 8) << 16 | (ix + 8) of the certified cell, or kFar
+    int l;           // its local pixel in the tile, or -1
 };
 
-__device__ __forceinline__ int tile_local(const TileView &v, int x, int y)
+// The hot path below is written branch-free (selects, non-short-circuit
+// predicates, predicated shared REDs): the ALU pipe, not fp64, bounds the
+// kernel (ncu), and every short-circuit branch costs a reconvergence pair.
+
+// Local pixel of in-frame cell (x, y) in the tile, or -1 (not owned).  rows
+// of an empty tile are never read (its items are never scheduled).
+__device__ __forceinline__ int tile_local(const TileView &v, int x, int y, bool ok)
 {
     const int r = y - v.y0;
-    if ((unsigned)r >= (unsigned)v.nrows) return -1;
+    ok = ok & ((unsigned)r < (unsigned)v.nrows);
+    const int rc = ok ? r : 0;
     int e0, e1, e2, e3;
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
-                 : "r"(v.rows + 16u * (unsigned)r));
+                 : "r"(v.rows + 16u * (unsigned)rc));
     const int xl = e0 & 0xffff, xh = (int)((unsigned)e0 >> 16);
     const int xl2 = e2 & 0xffff, xh2 = (int)((unsigned)e2 >> 16);
-    if (x >= xl && x <= xh) return e1 + x - xl;
-    if (x >= xl2 && x <= xh2) return e3 + x - xl2;
-    return -1;
+    const bool in1 = (x >= xl) & (x <= xh), in2 = (x >= xl2) & (x <= xh2);
+    const int l = in1 ? e1 + x - xl : (in2 ? e3 + x - xl2 : -1);
+    return ok ? l : -1;
 }
 
-__device__ __forceinline__ void tile_mark(unsigned img, int l)
+// red.shared of pixel l's u16 counter when `on`
+__device__ __forceinline__ void tile_mark(unsigned img, int l, bool on)
 {
-    EVD_CHECK(l >= 0 && l < 2 * kTileMaxWords);
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(img + 4u * (unsigned)(l >> 1)),
-                 "r"(1u << ((l & 1) << 4))
+    EVD_CHECK(!on || (l >= 0 && l < 2 * kTileMaxWords));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                 "@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(img + 4u * (unsigned)(l >> 1)),
+                 "r"(1u << ((l & 1) << 4)), "r"((unsigned)on)
                  : "memory");
 }
 
-__device__ __forceinline__ TilePoint tile_point(double x, double y, double t, double nu,
-                                                double rden, double cx, double cy, int W, int H,
-                                                const TileView &v)
+__device__ __forceinline__ bool sure_frac(float X, float m)
+{
+    const float f = X - floorf(X);
+    return (X >= 1.0f) & (X <= 32000.0f) & (f > m) & (f < 1.0f - 2.0f * m);
+}
+
+__device__ __forceinline__ TilePoint tile_point(float xf, float yf, double t, double nu,
+                                                double rden, float cxs, float cys, float K,
+                                                int W, int H, const TileView &v)
 {
     TilePoint p;
-    const Warped w = warp_approx(x, y, t, nu, rden, cx, cy);
-    p.x = w.x;
-    p.y = w.y;
-    p.m = sure_margin(w, cx, cy);
-    const double fx = floor(w.x), fy = floor(w.y);
-    const bool sure = w.x - p.m > fx && w.x + p.m < fx + 1.0 && w.y - p.m > fy &&
-                      w.y + p.m < fy + 1.0 && fx >= -2.0 && fx <= 32000.0 && fy >= -2.0 &&
-                      fy <= 32000.0;
-    p.code = kFar;
-    p.l = -1;
-    if (sure) {
-        const int ix = (int)fx, iy = (int)fy;
-        p.code = ((unsigned)(iy + 2) << 16) | (unsigned)(ix + 2);
-        if (ix >= 0 && ix < W && iy >= 0 && iy < H) p.l = tile_local(v, ix, iy);
-    }
+    const float s = __double2float_rn(dmul(dadd(1.0, dmul(nu, t)), rden));
+    p.x = fmaf(xf, s, cxs);
+    p.y = fmaf(yf, s, cys);
+    p.m = fmaf(fmaxf(fabsf(p.x), fabsf(p.y)), 1.9e-7f, K);
+    const bool sure = sure_frac(p.x, p.m) & sure_frac(p.y, p.m);
+    const int ix = sure ? (int)p.x : 0, iy = sure ? (int)p.y : 0;  // shifted cell, >= 1
+    p.code = sure ? (((unsigned)iy << 16) | (unsigned)ix) : kFar;
+    const bool in = sure & (ix >= 8) & (ix < W + 8) & (iy >= 8) & (iy < H + 8);
+    p.l = tile_local(v, ix - 8, iy - 8, in);
     return p;
 }
 
 __device__ __forceinline__ bool code_in_frame(unsigned c, int W, int H)
 {
-    const int fx = (int)(c & 0xffffu) - 2, fy = (int)(c >> 16) - 2;
-    return fx >= 0 && fx < W && fy >= 0 && fy < H;
+    const int fx = (int)(c & 0xffffu) - 8, fy = (int)(c >> 16) - 8;
+    return (fx >= 0) & (fx < W) & (fy >= 0) & (fy < H);
 }
 
 // Certified outcome of the segment a -> b (sure_segment_adj, evd_device.cuh,
-// from the points' certified cells): false if uncertain; else marks the
-// tile's pixels among the end cells and sets inside.
-__device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, int W, int H,
-                                          unsigned img, int &inside)
+// from the points' certified cells): false if uncertain; else (when `on`)
+// marks the tile's pixels among the end cells and sets inside.  Off the
+// frame: both endpoints beyond one edge by their error bound plus 1e-3 px,
+// which also covers the reference's clip rounding, (|ax| + |bx|) 2^-50 <
+// 1e-4 px while the endpoints stay below 1e11 px (checked; the comparisons'
+// own fp32 rounding near W + 8 is < 1.2e-4 px).
+__device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, float Wf,
+                                          float Hf, int W, int H, unsigned img, bool on,
+                                          int &inside)
 {
-    const double sx = a.m + b.m + 1e-12 * (1.0 + fabs(a.x) + fabs(b.x));
-    const double sy = a.m + b.m + 1e-12 * (1.0 + fabs(a.y) + fabs(b.y));
-    inside = 0;
-    if ((a.x < -sx && b.x < -sx) || (a.x > W + sx && b.x > W + sx) ||
-        (a.y < -sy && b.y < -sy) || (a.y > H + sy && b.y > H + sy))
-        return true;
-    if (a.code == kFar || b.code == kFar) return false;
+    const bool small = (fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(b.x), fabsf(b.y))) <
+                        1e11f);
+    const bool off = small & (((a.x + a.m < 7.999f) & (b.x + b.m < 7.999f)) |
+                              ((a.x - a.m > Wf + 8.001f) & (b.x - b.m > Wf + 8.001f)) |
+                              ((a.y + a.m < 7.999f) & (b.y + b.m < 7.999f)) |
+                              ((a.y - a.m > Hf + 8.001f) & (b.y - b.m > Hf + 8.001f)));
     const int dx = (int)(a.code & 0xffffu) - (int)(b.code & 0xffffu);
     const int dy = (int)(a.code >> 16) - (int)(b.code >> 16);
-    if (abs(dx) + abs(dy) > 1) return false;
-    inside = (code_in_frame(a.code, W, H) && code_in_frame(b.code, W, H)) ? 1 : 0;
-    if (a.l >= 0) tile_mark(img, a.l);
-    if (b.l >= 0 && b.code != a.code) tile_mark(img, b.l);
-    return true;
+    const bool cells = (a.code != kFar) & (b.code != kFar) & (abs(dx) + abs(dy) <= 1);
+    const bool sure = off | cells;
+    const bool mark = on & !off & cells;
+    inside = (mark & code_in_frame(a.code, W, H) & code_in_frame(b.code, W, H)) ? 1 : 0;
+    tile_mark(img, a.l, mark & (a.l >= 0));
+    tile_mark(img, b.l, mark & (b.l >= 0) & (b.code != a.code));
+    return sure;
 }
 
 // CONTIG: the intervals are contiguous (lo[k+1] == hi[k]); a group is 31
@@ -704,6 +742,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         }
         const double kappa = smax * (hypot(cx, cy) + 1.5) * 1e-12;
         const unsigned my_img = it.view.img + 4u * (unsigned)(lane * words);
+        const float cxs = (float)(cx + 8.0), cys = (float)(cy + 8.0);  // exact: halves < 2^23
+        const float Kxy = 1.25e-7f * fmaxf(cxs, cys) + 1e-9f;
+        const float Wf = (float)W, Hf = (float)H;
         unsigned long long fi = 0;
         int nq = 0, nx = 0;  // queued segments / uncertain pairs (warp-uniform)
         // Events in chunks of 32: lane l loads event l of the chunk (coalesced),
@@ -711,13 +752,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         // the surviving events, broadcasting each from its lane.
         for (int c0 = warp * 32; c0 < cn.y; c0 += kTileWarps * 32) {
             const int el_l = c0 + lane;
-            double xl = 0.0, yl = 0.0, tl = 0.0;
+            double tl = 0.0;
+            float2 xyl = make_float2(0.0f, 0.0f);
             bool need = false;
             if (el_l < cn.y) {
                 const long long e = it.e0 + el_l;
                 tl = __ldg(a.ts + e);
-                xl = __ldg(a.xs + e);
-                yl = __ldg(a.ys + e);
+                xyl = __ldg(a.xyf + e);
                 const double rho = (double)__ldg(a.rho + e);
                 const double smin = dmul(dadd(1.0, dmul(hmax, tl)), rhmax);
                 need = !(smin > rho * (1.0 + 1e-9) && rho > kappa);
@@ -727,10 +768,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
                 const int i = __ffs(todo) - 1;
                 todo &= todo - 1;
                 const int el = c0 + i;
-                const double x = __shfl_sync(0xffffffffu, xl, i);
-                const double y = __shfl_sync(0xffffffffu, yl, i);
+                const float x = __shfl_sync(0xffffffffu, xyl.x, i);
+                const float y = __shfl_sync(0xffffffffu, xyl.y, i);
                 const double tt = __shfl_sync(0xffffffffu, tl, i);
-                TilePoint pa = tile_point(x, y, tt, nu_a, rden_a, cx, cy, W, H, it.view);
+                TilePoint pa = tile_point(x, y, tt, nu_a, rden_a, cxs, cys, Kxy, W, H, it.view);
                 TilePoint pb;
                 if (CONTIG) {
                     pb.x = __shfl_down_sync(0xffffffffu, pa.x, 1);
@@ -739,17 +780,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
                     pb.code = __shfl_down_sync(0xffffffffu, pa.code, 1);
                     pb.l = __shfl_down_sync(0xffffffffu, pa.l, 1);
                 } else {
-                    pb = tile_point(x, y, tt, nu_b, rden_b, cx, cy, W, H, it.view);
+                    pb = tile_point(x, y, tt, nu_b, rden_b, cxs, cys, Kxy, W, H, it.view);
                 }
-                bool unc = false;
-                if (valid) {
-                    int ins;
-                    if (tile_pair(pa, pb, W, H, my_img, ins)) {
-                        if (el < cn.x) fi += ins;
-                    } else {
-                        unc = true;
-                    }
-                }
+                int ins;
+                const bool sure = tile_pair(pa, pb, Wf, Hf, W, H, my_img, valid, ins);
+                const bool unc = valid & !sure;
+                fi += (el < cn.x) ? ins : 0;
                 const unsigned bu = __ballot_sync(0xffffffffu, unc);
                 if (unc) wq.ev[nx + __popc(bu & ((1u << lane) - 1u))] = (el << 5) | lane;
                 nx += __popc(bu);
@@ -884,7 +920,8 @@ cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, cons
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return f->h_cnt[a].y > f->h_cnt[b].y; });
     if ((e = ensure(f->xs, f->xs_cap, total)) || (e = ensure(f->ys, f->ys_cap, total)) ||
-        (e = ensure(f->ts, f->ts_cap, total)) || (e = ensure(f->rho, f->rho_cap, total)))
+        (e = ensure(f->ts, f->ts_cap, total)) || (e = ensure(f->rho, f->rho_cap, total)) ||
+        (e = ensure(f->xyf, f->xyf_cap, total)))
         return e;
     if ((e = cudaMemcpyAsync(f->start, start.data(), T * sizeof(long long), cudaMemcpyHostToDevice, s)) ||
         (e = cudaMemcpyAsync(f->cnt, f->h_cnt.data(), T * sizeof(int2), cudaMemcpyHostToDevice, s)) ||
@@ -895,7 +932,7 @@ cudaError_t tiles_bin(FrontierTiles *f, const double *xc, const double *yc, cons
         return e;
     if (n > 0) {
         k_tile_fill<<<blocks, 256, 0, s>>>(xc, yc, t, n, g, W / 2.0, H / 2.0, f->cursor, f->xs,
-                                           f->ys, f->ts, f->rho);
+                                           f->ys, f->ts, f->rho, f->xyf);
         (*launches)++;
     }
     if ((e = cudaStreamSynchronize(s))) return e;  // host vectors above are freed on return
@@ -924,6 +961,7 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     a.ys = f->ys;
     a.ts = f->ts;
     a.rho = f->rho;
+    a.xyf = f->xyf;
     a.start = f->start;
     a.cnt = f->cnt;
     a.meta = f->meta;
