@@ -484,6 +484,8 @@ struct TileArgs {
     const double *lo, *hi, *den_lo, *den_hi;
     double cx, cy;
     int W, H, words;
+    float cxs, cys, Kxy, Wf, Hf;  // tile_point / tile_pair constants (kernel parameters:
+                                  // read as constant-bank operands, no registers)
     unsigned int *ctr;
     unsigned long long *fi_out, *marks_s;
 };
@@ -565,9 +567,9 @@ constexpr unsigned kFar = 0xffffffffu;
 // f = X - floor(X) (exact: Sterbenz) has f > m and f < 1 - 2m (RN32(1 - 2m)
 // errs by <= 2^-25 < m since m >= 1.9e-7).
 struct TilePoint {
-    float x, y, m;   // shifted position (+8) and its error bound
     unsigned code;   // (iy + 8) << 16 | (ix + 8) of the certified cell, or kFar
     int l;           // its local pixel in the tile, or -1
+    int out;         // certainly beyond the left / right / top / bottom edge (bits 0-3)
 };
 
 // The hot path below is written branch-free (selects, non-short-circuit
@@ -610,15 +612,23 @@ __device__ __forceinline__ bool sure_frac(float X, float m)
 
 __device__ __forceinline__ TilePoint tile_point(float xf, float yf, double t, double nu,
                                                 double rden, float cxs, float cys, float K,
-                                                int W, int H, const TileView &v)
+                                                float Wf, float Hf, int W, int H,
+                                                const TileView &v)
 {
     TilePoint p;
     const float s = __double2float_rn(dmul(dadd(1.0, dmul(nu, t)), rden));
-    p.x = fmaf(xf, s, cxs);
-    p.y = fmaf(yf, s, cys);
-    p.m = fmaf(fmaxf(fabsf(p.x), fabsf(p.y)), 1.9e-7f, K);
-    const bool sure = sure_frac(p.x, p.m) & sure_frac(p.y, p.m);
-    const int ix = sure ? (int)p.x : 0, iy = sure ? (int)p.y : 0;  // shifted cell, >= 1
+    const float X = fmaf(xf, s, cxs), Y = fmaf(yf, s, cys);
+    const float mag = fmaxf(fabsf(X), fabsf(Y));
+    const float m = fmaf(mag, 1.9e-7f, K);
+    // Beyond an edge by the error bound plus 1e-3 px, which also covers the
+    // reference's clip rounding, (|ax| + |bx|) 2^-50 < 1e-4 px while the
+    // endpoints stay below 1e11 px (else no bit); the comparisons' own fp32
+    // rounding near W + 8 is < 1.2e-4 px.
+    const bool small = mag < 1e11f;
+    p.out = (small & (X + m < 7.999f) ? 1 : 0) | (small & (X - m > Wf + 8.001f) ? 2 : 0) |
+            (small & (Y + m < 7.999f) ? 4 : 0) | (small & (Y - m > Hf + 8.001f) ? 8 : 0);
+    const bool sure = sure_frac(X, m) & sure_frac(Y, m);
+    const int ix = sure ? (int)X : 0, iy = sure ? (int)Y : 0;  // shifted cell, >= 1
     p.code = sure ? (((unsigned)iy << 16) | (unsigned)ix) : kFar;
     const bool in = sure & (ix >= 8) & (ix < W + 8) & (iy >= 8) & (iy < H + 8);
     p.l = tile_local(v, ix - 8, iy - 8, in);
@@ -634,20 +644,11 @@ __device__ __forceinline__ bool code_in_frame(unsigned c, int W, int H)
 // Certified outcome of the segment a -> b (sure_segment_adj, evd_device.cuh,
 // from the points' certified cells): false if uncertain; else (when `on`)
 // marks the tile's pixels among the end cells and sets inside.  Off the
-// frame: both endpoints beyond one edge by their error bound plus 1e-3 px,
-// which also covers the reference's clip rounding, (|ax| + |bx|) 2^-50 <
-// 1e-4 px while the endpoints stay below 1e11 px (checked; the comparisons'
-// own fp32 rounding near W + 8 is < 1.2e-4 px).
-__device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, float Wf,
-                                          float Hf, int W, int H, unsigned img, bool on,
-                                          int &inside)
+// frame: both endpoints beyond one edge (their `out` bits).
+__device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, int W, int H,
+                                          unsigned img, bool on, int &inside)
 {
-    const bool small = (fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(b.x), fabsf(b.y))) <
-                        1e11f);
-    const bool off = small & (((a.x + a.m < 7.999f) & (b.x + b.m < 7.999f)) |
-                              ((a.x - a.m > Wf + 8.001f) & (b.x - b.m > Wf + 8.001f)) |
-                              ((a.y + a.m < 7.999f) & (b.y + b.m < 7.999f)) |
-                              ((a.y - a.m > Hf + 8.001f) & (b.y - b.m > Hf + 8.001f)));
+    const bool off = (a.out & b.out) != 0;
     const int dx = (int)(a.code & 0xffffu) - (int)(b.code & 0xffffu);
     const int dy = (int)(a.code >> 16) - (int)(b.code >> 16);
     const bool cells = (a.code != kFar) & (b.code != kFar) & (abs(dx) + abs(dy) <= 1);
@@ -742,9 +743,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
         }
         const double kappa = smax * (hypot(cx, cy) + 1.5) * 1e-12;
         const unsigned my_img = it.view.img + 4u * (unsigned)(lane * words);
-        const float cxs = (float)(cx + 8.0), cys = (float)(cy + 8.0);  // exact: halves < 2^23
-        const float Kxy = 1.25e-7f * fmaxf(cxs, cys) + 1e-9f;
-        const float Wf = (float)W, Hf = (float)H;
+        const float cxs = a.cxs, cys = a.cys, Kxy = a.Kxy, Wf = a.Wf, Hf = a.Hf;
         unsigned long long fi = 0;
         int nq = 0, nx = 0;  // queued segments / uncertain pairs (warp-uniform)
         // Events in chunks of 32: lane l loads event l of the chunk (coalesced),
@@ -771,19 +770,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_frontier_tiles(TileArgs a)
                 const float x = __shfl_sync(0xffffffffu, xyl.x, i);
                 const float y = __shfl_sync(0xffffffffu, xyl.y, i);
                 const double tt = __shfl_sync(0xffffffffu, tl, i);
-                TilePoint pa = tile_point(x, y, tt, nu_a, rden_a, cxs, cys, Kxy, W, H, it.view);
+                TilePoint pa = tile_point(x, y, tt, nu_a, rden_a, cxs, cys, Kxy, Wf, Hf, W, H,
+                                          it.view);
                 TilePoint pb;
                 if (CONTIG) {
-                    pb.x = __shfl_down_sync(0xffffffffu, pa.x, 1);
-                    pb.y = __shfl_down_sync(0xffffffffu, pa.y, 1);
-                    pb.m = __shfl_down_sync(0xffffffffu, pa.m, 1);
                     pb.code = __shfl_down_sync(0xffffffffu, pa.code, 1);
                     pb.l = __shfl_down_sync(0xffffffffu, pa.l, 1);
+                    pb.out = __shfl_down_sync(0xffffffffu, pa.out, 1);
                 } else {
-                    pb = tile_point(x, y, tt, nu_b, rden_b, cxs, cys, Kxy, W, H, it.view);
+                    pb = tile_point(x, y, tt, nu_b, rden_b, cxs, cys, Kxy, Wf, Hf, W, H, it.view);
                 }
                 int ins;
-                const bool sure = tile_pair(pa, pb, Wf, Hf, W, H, my_img, valid, ins);
+                const bool sure = tile_pair(pa, pb, W, H, my_img, valid, ins);
                 const bool unc = valid & !sure;
                 fi += (el < cn.x) ? ins : 0;
                 const unsigned bu = __ballot_sync(0xffffffffu, unc);
@@ -978,6 +976,11 @@ cudaError_t tiles_eval(FrontierTiles *f, const double *lo, const double *hi, con
     a.cy = f->H / 2.0;
     a.W = f->W;
     a.H = f->H;
+    a.cxs = (float)(a.cx + 8.0);  // exact: multiples of 1/2 below 2^23
+    a.cys = (float)(a.cy + 8.0);
+    a.Kxy = 1.25e-7f * std::max(a.cxs, a.cys) + 1e-9f;
+    a.Wf = (float)f->W;
+    a.Hf = (float)f->H;
     a.words = tile_words(f->P);
     a.ctr = f->ctr;
     a.fi_out = fi_out;
