@@ -49,7 +49,10 @@
 namespace evd {
 
 constexpr double kTileDelta = 0.75;  // > sqrt(2)/2 + rounding of the sampled positions
-constexpr int kTileThreads = 512;
+#ifndef EVD_TILE_THREADS
+#define EVD_TILE_THREADS 512
+#endif
+constexpr int kTileThreads = EVD_TILE_THREADS;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kTileMaxEvents = 65535;  // u16 counters
 constexpr int kTileMaxWords = 32768;   // bound on a tile image's words (checked builds)
