@@ -914,7 +914,7 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     // groups have little fixed cost to save)
     int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? (max_n < kSmallWindow ? 3 : 4) : 1;
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
-    if (ctx->trace_on) spec_k = 1;
+    if (ctx->trace_on && !getenv("EVD_TRACE_SPEC")) spec_k = 1;  // EVD_TRACE_SPEC=1: rounds
     // CTA size: small windows on the whole grid are latency-bound (384 fatter
     // threads), large ones sampler-throughput-bound (768); grouped solves and
     // the traced build stay at 512 (measured: cfg 1 1.10 -> 1.04 ms at 384,

@@ -1589,11 +1589,26 @@ struct SpecState {
     int rounds;
 };
 
+// Frontier entries already chosen for a speculative slot carry this bit in
+// their counter (set by the round's slot selection, masked wherever the
+// counter is compared or copied), so the selection skips them in O(1)
+// instead of searching the result cache per entry.
+constexpr long long kSpecFlag = 1ll << 62;
+
+// the result-cache index holding `counter`, or -1 (all 32 lanes of warp 0)
 __device__ __forceinline__ int spec_find(const SpecState &Z, long long counter)
 {
-    for (int k = 0; k < Z.ncache; k++)
-        if (Z.cache[k].counter == counter) return k;
-    return -1;
+    const int lane = threadIdx.x & 31, nc = Z.ncache;
+    int hit = -1;
+    for (int k0 = 0; k0 < nc; k0 += 32) {
+        const bool m = k0 + lane < nc && Z.cache[k0 + lane].counter == counter;
+        const unsigned b = __ballot_sync(0xffffffffu, m);
+        if (b) {
+            hit = k0 + __ffs(b) - 1;
+            break;
+        }
+    }
+    return hit;
 }
 
 // warp-0 argmax over the shared frontier, skipping entries flagged by `skip`
@@ -1605,7 +1620,8 @@ __device__ __forceinline__ long long spec_argmax(const FrontierEntry *fr, long l
     for (long long i = threadIdx.x & 31; i < n; i += 32) {
         const FrontierEntry &e = fr[i];
         if (skip(e)) continue;
-        if (bi < 0 || better(e.bound, e.counter, bb, bc)) { bb = e.bound; bc = e.counter; bi = i; }
+        const long long ec = e.counter & ~kSpecFlag;
+        if (bi < 0 || better(e.bound, ec, bb, bc)) { bb = e.bound; bc = ec; bi = i; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1627,7 +1643,7 @@ __device__ __forceinline__ void spec_set_slot(const SolveArgs &a, SpecSlot &s,
     s.den_lo = dadd(1.0, dmul(e.lo, a.tau));
     s.den_c = dadd(1.0, dmul(c, a.tau));
     s.den_hi = dadd(1.0, dmul(e.hi, a.tau));
-    s.counter = e.counter;
+    s.counter = e.counter & ~kSpecFlag;
 }
 
 template <int NT>
@@ -1677,6 +1693,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
             continue;
         }
         const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
+        if (kTraceBuild && a.trace && grp == 0 && w == 0 && gb == 0) trace_point(a, 0, -1);
         grid_sync(ctr, target, GB);
         if (gb == 0 && threadIdx.x == 0) {
             unsigned long long *z = &st->sacc[0][0][0];
@@ -1700,6 +1717,11 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
         while (!Z.done) {
             const int ns = Z.nslot, mode = Z.mode, par = Z.parity;
             unsigned long long (*sacc)[8] = st->sacc[par];
+            // round timeline (trace build, window 0 of group 0): the same
+            // slots as k_solve's per-node trace, one entry per round
+            const long long it = Z.rounds;
+            const bool tr = kTraceBuild && a.trace && grp == 0 && w == 0;
+            if (tr && gb == 0) trace_point(a, it, kTrB0Top);
             if (threadIdx.x < kSpecK * 5) (&s_acc[0][0])[threadIdx.x] = 0;
             __syncthreads();
             // events: one pass per slot (each with its own work counter)
@@ -1722,12 +1744,15 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 }
             }
             __syncthreads();
+            if (tr && gb == 0) trace_point(a, it, kTrB0Events);
+            if (tr) trace_max(a, it, kTrEventsMax);
             if (threadIdx.x < ns * 5) {
                 const int s = threadIdx.x / 5, k = threadIdx.x % 5;
                 const unsigned long long x = s_acc[s][k];
                 if (x) atomicAdd(&sacc[s][k == 4 ? 6 : k], x);
             }
             grid_sync(ctr, target, GB);
+            if (tr && gb == 0) trace_point(a, it, kTrB0Pixels0);
 
             // pixels: per-slot accumulators, the point images' cut walks beside
             // the segment images' sums of squares
@@ -1782,7 +1807,13 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                     if (x) atomicAdd(&sacc[k >> 1][4 + (k & 1)], x);
                 }
             }
+            if (tr) {
+                __syncthreads();
+                if (gb == 0) trace_point(a, it, kTrB0Pixels1);
+                trace_max(a, it, kTrPixelsMax);
+            }
             grid_sync(ctr, target, GB);
+            if (tr && gb == 0) trace_point(a, it, kTrB0Step0);
 
             // step: finish every slot's contrast and bounds, then replay the
             // reference's pops while their results are known
@@ -1813,6 +1844,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                     const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
                     const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
                     Z.marks += a0 + a23.y;
+                    if (tr && gb == 0 && it < a.trace_iters)  // round's marks, slots
+                        a.trace[1 + kTraceSlots * it + kTrMarks] += (long long)(a0 + a23.y);
                     Z.exact += a6;
                     const double Cs = ddiv(dadd(0.0, Sv), Md);  // np.sum(...) / M
                     const double cbA = dsub(ddiv((double)a45.x, Md), __ldg(a.pow2 + Z.fiA[s]));
@@ -1894,9 +1927,10 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                     const long long bi = spec_argmax(frs, Z.fr_n, [](const FrontierEntry &) {
                         return false;
                     });
-                    int hit = -1;
+                    const FrontierEntry top = frs[bi];
+                    const int hit = spec_find(Z, top.counter & ~kSpecFlag);
+                    __syncwarp();
                     if (lane == 0) {
-                        const FrontierEntry top = frs[bi];
                         frs[bi] = frs[Z.fr_n - 1];  // swap-remove
                         Z.fr_n--;
                         Z.iterations++;
@@ -1905,7 +1939,6 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                             Z.bound_gap = (0.0 > gap) ? 0.0 : gap;
                             stop = 1;
                         } else {
-                            hit = spec_find(Z, top.counter);
                             spec_set_slot(a, node, top);
                             if (hit >= 0) Z.cur = hit;
                             else next_uncached = 1;
@@ -1944,13 +1977,14 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                             if (dsub(e.bound, Z.c_hat) <= a.gamma ||
                                 dsub(e.hi, e.lo) < a.min_width)
                                 return true;
-                            for (int q = 0; q < Z.nslot; q++)
-                                if (Z.slot[q].counter == e.counter) return true;
-                            return spec_find(Z, e.counter) >= 0;
+                            // evaluated or scheduled already (its result is
+                            // cached, or it is one of this round's slots)
+                            return (e.counter & kSpecFlag) != 0;
                         });
                         if (bi < 0) break;
                         if (lane == 0) {
                             spec_set_slot(a, Z.slot[Z.nslot], frs[bi]);
+                            frs[bi].counter |= kSpecFlag;
                             Z.nslot++;
                         }
                         __syncwarp();
@@ -1959,6 +1993,11 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 }
             }
             __syncthreads();
+            if (tr && gb == 0) {
+                trace_point(a, it, kTrB0Step1);
+                if (threadIdx.x == 0 && it < a.trace_iters)
+                    a.trace[1 + kTraceSlots * it + kTrExact] = ns;  // slots this round
+            }
         }
         // speculative slots' point images are summed (and cleared) every round;
         // segment images are cleared by the pixel phase: nothing is left dirty

@@ -1,6 +1,9 @@
 """Per-iteration device timeline of one evd_solve (globaltimer trace).
 
-python tools/trace_solve.py [cfg] [repeats] [--all]
+python tools/trace_solve.py [cfg] [repeats] [--all] [--spec]
+--spec: the speculative-round kernel (k_solve_spec, the default solve), one
+row per round (several node evaluations); Mmarks = the round's marks,
+"exact%" column replaced by the round's slots.
 Per node evaluation (us, from block 0's start of the node):
   b0ev  block 0's events      maxev  the slowest block's events
   bar1  last events -> block 0 leaves barrier 1
@@ -20,6 +23,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["EVD_TRACE"] = "1"  # read when the libevd context is created
+SPEC = "--spec" in sys.argv
+if SPEC:
+    os.environ["EVD_TRACE_SPEC"] = "1"
 # the probes are compiled only into the diagnostic build
 os.environ.setdefault("EVD_LIB", os.path.join(ROOT, "paper_2209_13168_b200", "libevd_trace.so"))
 
@@ -52,7 +58,8 @@ def main():
     k = (len(tr) - 1) // SLOTS
     raw = tr[1:1 + SLOTS * k].reshape(k, SLOTS)
     T = raw[:, :8].astype(np.float64) / 1e3
-    k = min(k, st.point_evals)
+    res, _ = sol.solve_loaded(_lib.context(), evd.SolverParams())
+    k = min(k, res.rounds if SPEC else st.point_evals)
     cols = {
         "b0ev": T[:k, 1] - T[:k, 0],
         "maxev": T[:k, 2] - T[:k, 0],
@@ -64,12 +71,15 @@ def main():
         "total": np.r_[T[1:k, 0] - T[:k - 1, 0], np.nan],
         "Mmarks": raw[:k, 8] / 1e6,
         "G/s": raw[:k, 8] / (T[:k, 2] - T[:k, 0]) / 1e3,  # segment marks / event phase
-        "exact%": 100.0 * raw[:k, 9] / b.n,
     }
-    res, _ = sol.solve_loaded(_lib.context(), evd.SolverParams())
+    if SPEC:
+        cols["slots"] = raw[:k, 9].astype(np.float64)
+    else:
+        cols["exact%"] = 100.0 * raw[:k, 9] / b.n
     print(f"cfg {cfg}: n={b.n} iterations={r.iterations} device_ms={st.device_ms:.3f} "
+          f"rounds={res.rounds} "
           f"exact-path share={res.exact_events / (b.n * res.point_evals):.3f}")
-    print("node " + " ".join(f"{c:>8s}" for c in cols))
+    print(("round" if SPEC else "node ") + " ".join(f"{c:>8s}" for c in cols))
     show = range(k) if "--all" in sys.argv else list(range(min(k, 12))) + list(range(max(12, k - 6), k))
     for i in show:
         print(f"{i:4d} " + " ".join(f"{cols[c][i]:8.1f}" for c in cols))
