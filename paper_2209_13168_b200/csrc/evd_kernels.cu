@@ -1756,19 +1756,17 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
 
             // pixels: per-slot accumulators, the point images' cut walks beside
             // the segment images' sums of squares
-            if (threadIdx.x == 0) {
-                for (int s = 0; s < ns; s++) {
-                    const ulonglong2 a01 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s]));
-                    const unsigned long long a2 = __ldcg(&sacc[s][2]);
-                    Z.mu[s] = ddiv((double)a01.x, (double)M);
-                    Z.fiA[s] = a01.y;
-                    Z.fiB[s] = a2;
-                }
-                if (gb == 0) {
-                    unsigned long long *nxt = &st->sacc[par ^ 1][0][0];
-                    for (int k = 0; k < kSpecK * 8; k++) __stcg(nxt + k, 0ull);
-                }
+            // one thread per slot (the loads in parallel, not one after another)
+            if (threadIdx.x < ns) {
+                const int s = threadIdx.x;
+                const ulonglong2 a01 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s]));
+                const unsigned long long a2 = __ldcg(&sacc[s][2]);
+                Z.mu[s] = ddiv((double)a01.x, (double)M);
+                Z.fiA[s] = a01.y;
+                Z.fiB[s] = a2;
             }
+            if (gb == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + kSpecK * 8)
+                __stcg(&st->sacc[par ^ 1][0][0] + (threadIdx.x - 32), 0ull);
             __syncthreads();
             if (threadIdx.x < kPixCutThreads) {
                 for (int p = gb; p < ns * C; p += GB) {
@@ -1835,21 +1833,31 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 }
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
+            // each slot's contrast and child bounds, one thread per slot
+            __shared__ double s_res[kSpecK][3];
+            __shared__ unsigned long long s_cnt[kSpecK][2];
+            if (threadIdx.x < ns) {
+                const int s = threadIdx.x;
                 const double Md = (double)M;
+                const double Sv = scratch[s * (C + ntop) + (C > 1 ? tree.top_root : 0)];
+                const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
+                const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
+                const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
+                s_cnt[s][0] = a0 + a23.y;
+                s_cnt[s][1] = a6;
+                s_res[s][0] = ddiv(dadd(0.0, Sv), Md);  // np.sum(...) / M
+                s_res[s][1] = dsub(ddiv((double)a45.x, Md), __ldg(a.pow2 + Z.fiA[s]));
+                s_res[s][2] = dsub(ddiv((double)a45.y, Md), __ldg(a.pow2 + Z.fiB[s]));
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
                 Z.rounds++;
                 for (int s = 0; s < ns; s++) {
-                    const double Sv = scratch[s * (C + ntop) + (C > 1 ? tree.top_root : 0)];
-                    const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
-                    const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
-                    const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
-                    Z.marks += a0 + a23.y;
+                    Z.marks += s_cnt[s][0];
                     if (tr && gb == 0 && it < a.trace_iters)  // round's marks, slots
-                        a.trace[1 + kTraceSlots * it + kTrMarks] += (long long)(a0 + a23.y);
-                    Z.exact += a6;
-                    const double Cs = ddiv(dadd(0.0, Sv), Md);  // np.sum(...) / M
-                    const double cbA = dsub(ddiv((double)a45.x, Md), __ldg(a.pow2 + Z.fiA[s]));
-                    const double cbB = dsub(ddiv((double)a45.y, Md), __ldg(a.pow2 + Z.fiB[s]));
+                        a.trace[1 + kTraceSlots * it + kTrMarks] += (long long)s_cnt[s][0];
+                    Z.exact += s_cnt[s][1];
+                    const double Cs = s_res[s][0], cbA = s_res[s][1], cbB = s_res[s][2];
                     if (s == 0 && mode == kModeRoot) {
                         Z.S[0] = Cs;
                         Z.mu[0] = cbA;  // the root bound
