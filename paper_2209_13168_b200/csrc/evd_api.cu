@@ -877,7 +877,10 @@ namespace {
 // chunks; it now measures 1-3% slower at every size (cfg 1, 2, 3, 5), so it is
 // off unless EVD_SOLVE_FILTER=1 (kept: tested, and a base for other targets).
 constexpr long long kFilterMinEvents = LLONG_MAX;
-constexpr long long kSpecMaxEvents = 2000000;  // speculative rounds for windows below this
+// 4 speculative slots below this, 2 above (cfg 5, 5.33 M events: 1 slot
+// 138.1 ms, 2 slots 135.8, 3 137.4, 4 136.2 -- measured after the round-2
+// step changes; before them 1 slot was best there)
+constexpr long long kSpecMaxEvents = 2000000;
 // CTA-size / slot-count policy for a whole-grid solve, from
 // tools/threshold_sweep.py (subsampled cfg 2 / cfg 3 windows and cfg 1):
 // 384 threads + 3 slots win at 20 k events, 512 + 4 slots at 50-150 k,
@@ -909,10 +912,10 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
     // trace is on (k_solve has the probes)
     // (on the whole grid: 3 slots measured best with 384-thread CTAs, 4 above,
-    // up to 2 M events -- cfg 3 20.07 -> 19.86 ms; at cfg 5 (5.3 M) the wide nodes
-    // make speculation cost more than the rounds it saves, and small CTA
-    // groups have little fixed cost to save)
-    int spec_k = (max_n < kSpecMaxEvents && GB >= 32) ? (max_n < kSmallWindow ? 3 : 4) : 1;
+    // up to 2 M events -- cfg 3 20.07 -> 19.86 ms; 2 at cfg 5 (5.3 M), where
+    // the wide nodes leave less fixed cost to save; small CTA groups have
+    // little fixed cost to save)
+    int spec_k = GB < 32 ? 1 : (max_n < kSmallWindow ? 3 : (max_n < kSpecMaxEvents ? 4 : 2));
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
     if (ctx->trace_on && !getenv("EVD_TRACE_SPEC")) spec_k = 1;  // EVD_TRACE_SPEC=1: rounds
     // CTA size: small windows on the whole grid are latency-bound (384 fatter
