@@ -199,3 +199,23 @@ def test_cfg3_frontier_sample_vs_oracle():
     # size-independent property: adjacent-leaf unions bound each leaf (marks >= 0,
     # fully_inside <= events)
     assert (fi <= b.n).all()
+
+
+@pytest.mark.parametrize("k", [1, 2, 30, 31, 32, 33, 62, 63, 64, 65, 97])
+def test_tiled_frontier_group_edges(frontier_path, k):
+    """Group boundaries of the tiled kernel (31 contiguous / 32 general
+    intervals per warp): contiguous frontiers of every awkward size, the same
+    intervals shuffled (non-contiguous), and zero-width intervals inside a
+    contiguous run, all against the per-interval kernel."""
+    from paper_2209_13168_b200 import _lib
+    b = synth.random_window(np.random.default_rng(k), 96, 72, 6000)
+    dom = velocity_domain(b.tau)
+    edges = np.linspace(dom.lo, -0.05, k + 1)
+    edges[k // 2] = edges[k // 2 + 1] if k > 2 else edges[k // 2]  # a zero-width interval
+    lo, hi = edges[:-1].copy(), edges[1:].copy()
+    perm = np.random.default_rng(k + 1).permutation(k)
+    frontier_path.set_option("frontier_path", _lib.FRONTIER_TILES)
+    for l, h in ((lo, hi), (lo[perm], hi[perm])):
+        got = con.frontier_terms(b, l, h, ctx=frontier_path)
+        want = con.bound_terms_many(b, l, h, ctx=frontier_path)
+        assert all(np.array_equal(u, v) for u, v in zip(got, want[:3]))
