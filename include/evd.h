@@ -68,6 +68,15 @@ int evd_device_sms(const evd_ctx *ctx);
 int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
                    int32_t width, int32_t height, double tau);
 
+/* k windows given as separate host arrays, resident as one concatenation (window
+ * w at offset counts[0] + ... + counts[w-1]) for evd_solve_windows: the arrays
+ * are gathered through pinned staging while the previous chunk is copied, with
+ * no host-side concatenation (estimate_stream_divergence, solver.py:139-162,
+ * over a list of EventBatch). */
+int evd_set_events_list(evd_ctx *ctx, const double *const *x, const double *const *y,
+                        const double *const *t, const int64_t *counts, int32_t k, int32_t width,
+                        int32_t height, double tau);
+
 /* ---- motion model ------------------------------------------------------ */
 /* radial_warp (geometry.py:78-87) of n arbitrary points. */
 int evd_radial_warp(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,

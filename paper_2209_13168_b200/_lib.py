@@ -26,7 +26,8 @@ FRONTIER_AUTO, FRONTIER_TILES, FRONTIER_GLOBAL, FRONTIER_GLOBAL_EXACT = 0, 1, 2,
 SYMBOLS = (
     "evd_create", "evd_destroy", "evd_last_error", "evd_set_stream", "evd_kernel_launches",
     "evd_window_generation",
-    "evd_device_sms", "evd_set_events", "evd_radial_warp", "evd_warp_scale",
+    "evd_device_sms", "evd_set_events", "evd_set_events_list", "evd_radial_warp",
+    "evd_warp_scale",
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_set_option",
     "evd_frontier_info", "evd_image_contrast",
     "evd_rasterize_segments",
@@ -92,6 +93,8 @@ _SIGS = {
     "evd_window_generation": (_i64, [_vp]),
     "evd_device_sms": (ctypes.c_int, [_vp]),
     "evd_set_events": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64]),
+    "evd_set_events_list": (ctypes.c_int, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_d),
+                                           ctypes.POINTER(_d), _i64p, _i32, _i32, _i32, _f64]),
     "evd_radial_warp": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _f64, _f64, _i32, _i32, _d, _d]),
     "evd_warp_scale": (ctypes.c_int, [_vp, _d, _i64, _f64, _f64, _d]),
     "evd_point_images": (ctypes.c_int, [_vp, _d, _i32, _i64p, _d, _u32p]),

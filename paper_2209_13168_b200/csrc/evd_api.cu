@@ -118,6 +118,10 @@ struct evd_ctx {
     int frontier_path = EVD_FRONTIER_AUTO;    // evd_set_option("frontier_path")
     long long frontier_budget = 8ll << 30;    // image bytes of the global-image paths
     int last_frontier_path = -1;
+    // pinned staging for evd_set_events_list (two halves, double-buffered)
+    unsigned char *stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -484,6 +488,9 @@ void evd_destroy(evd_ctx *ctx)
     tp.top.release();
     tp.cutval.release();
     tiles_free(ctx->tiles);
+    if (ctx->stage) cudaFreeHost(ctx->stage);
+    for (cudaEvent_t e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -531,6 +538,83 @@ int evd_set_events(evd_ctx *ctx, const double *x, const double *y, const double 
         LAUNCHED(1);
         // inputs are never retained (evd.h): the caller may reuse or free
         // x, y, t (pinned host or device memory) once this call returns
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->n = n;
+    ctx->gen++;
+    ctx->W = width;
+    ctx->H = height;
+    ctx->tau = tau;
+    return EVD_OK;
+}
+
+int evd_set_events_list(evd_ctx *ctx, const double *const *x, const double *const *y,
+                        const double *const *t, const int64_t *counts, int32_t k, int32_t width,
+                        int32_t height, double tau)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (k < 0 || width < 1 || height < 1 || (k > 0 && (!x || !y || !t || !counts)))
+        return fail(ctx, EVD_ERR_ARG, "bad evd_set_events_list arguments");
+    if (int rc = check_frame(ctx, width, height)) return rc;
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "batch duration tau must be positive");
+    long long n = 0;
+    for (int w = 0; w < k; w++) {
+        if (counts[w] < 0 || (counts[w] > 0 && (!x[w] || !y[w] || !t[w])))
+            return fail(ctx, EVD_ERR_ARG, "bad window %d", w);
+        n += counts[w];
+    }
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->xc.ensure(n));
+    CU(ctx->yc.ensure(n));
+    CU(ctx->t.ensure(n));
+    // Host windows are gathered into two pinned halves while the other half's
+    // copy runs: one host pass over the data, no host-side concatenation.
+    const size_t half = 16u << 20;
+    if (!ctx->stage) {
+        CU(cudaHostAlloc(&ctx->stage, 2 * half, cudaHostAllocDefault));
+        ctx->stage_bytes = 2 * half;
+        CU(cudaEventCreateWithFlags(&ctx->stage_ev[0], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ctx->stage_ev[1], cudaEventDisableTiming));
+    }
+    int cur = 0;
+    size_t fill = 0;
+    double *dst = nullptr;
+    long long dpos = 0;  // element offset in dst of the half being filled
+    auto flush = [&]() -> int {
+        if (!fill) return EVD_OK;
+        CU(cudaMemcpyAsync(dst + dpos, ctx->stage + cur * half, fill, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CU(cudaEventRecord(ctx->stage_ev[cur], ctx->stream));
+        dpos += fill / sizeof(double);
+        fill = 0;
+        cur ^= 1;
+        CU(cudaEventSynchronize(ctx->stage_ev[cur]));  // the next half is free again
+        return EVD_OK;
+    };
+    for (int a = 0; a < 3 && n > 0; a++) {
+        const double *const *src = a == 0 ? x : (a == 1 ? y : t);
+        dst = a == 0 ? ctx->xc.p : (a == 1 ? ctx->yc.p : ctx->t.p);
+        dpos = 0;
+        for (int w = 0; w < k; w++) {
+            size_t left = (size_t)counts[w] * sizeof(double);
+            const unsigned char *p = reinterpret_cast<const unsigned char *>(src[w]);
+            while (left) {
+                const size_t take = std::min(left, half - fill);
+                memcpy(ctx->stage + cur * half + fill, p, take);
+                fill += take;
+                p += take;
+                left -= take;
+                if (fill == half) {
+                    if (int rc = flush()) return rc;
+                }
+            }
+        }
+        if (int rc = flush()) return rc;
+    }
+    if (n > 0) {
+        launch_center(ctx->xc.p, ctx->yc.p, n, width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p,
+                      ctx->stream);
+        LAUNCHED(1);
         CU(cudaStreamSynchronize(ctx->stream));
     }
     ctx->n = n;

@@ -14,7 +14,6 @@ import ctypes
 import logging
 import time
 from dataclasses import dataclass
-from types import SimpleNamespace
 
 import numpy as np
 
@@ -160,9 +159,17 @@ def solve_windows(batches: list[EventBatch], params: SolverParams, groups: int =
     sizes = np.array([b.n for b in batches], dtype=np.int64)
     offsets = np.zeros(len(batches) + 1, dtype=np.int64)
     np.cumsum(sizes, out=offsets[1:])
-    cat = lambda k: np.concatenate([np.asarray(getattr(b, k), dtype=np.float64) for b in batches])
-    ctx = load_window(SimpleNamespace(x=cat("x"), y=cat("y"), t=cat("t"), tau=tau, geometry=g0),
-                      ctx)
+    ctx = ctx or _lib.context()
+    # every window's arrays straight to the device (evd_set_events_list: pinned
+    # staging, no host concatenation)
+    cols = [[_lib.f64(getattr(b, k)) for b in batches] for k in ("x", "y", "t")]
+    ptrs = [(_lib._d * len(batches))(*[_lib.ptr(a) for a in col]) for col in cols]
+    rc = ctx.lib.evd_set_events_list(ctx.h, ptrs[0], ptrs[1], ptrs[2],
+                                     _lib.ptr(sizes, _lib._i64p), len(batches), g0.width,
+                                     g0.height, tau)
+    if rc:
+        _raise(ctx, rc)
+    ctx._resident = None
     p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
                          float(params.min_interval_width), int(params.max_iterations))
     res = (_lib.WindowResult * len(batches))()
