@@ -72,18 +72,21 @@ def _same_window(ctx, key, arrays) -> bool:
                for a, c in zip(arrays, res[2]))
 
 
-def load_window(batch: EventBatch, ctx=None):
+def load_window(batch: EventBatch, ctx=None, cache: bool = True):
     """Make the window resident on the device (evd_set_events); returns the
     context.  The per-call entry points (accumulate_image, contrast_at,
     upper_bound_image, bound_terms, ...) call it every time, as the reference
     recomputes from the batch every time; a window already resident with
-    identical contents is not uploaded again (_same_window)."""
+    identical contents is not uploaded again (_same_window).  ``cache=False``
+    (one-shot callers such as a whole solve) uploads without keeping the host
+    copy the content check needs."""
     ctx = ctx or _lib.context()
     g = batch.geometry
     x, y, t = _lib.f64(batch.x), _lib.f64(batch.y), _lib.f64(batch.t)
     key = (x.ctypes.data, y.ctypes.data, t.ctypes.data, t.size, g.width, g.height,
            float(batch.tau))
-    if _same_window(ctx, key, (x, y, t)):
+    cache = cache and WINDOW_CACHE
+    if cache and _same_window(ctx, key, (x, y, t)):
         return ctx
     ctx._resident = None
     rc = ctx.lib.evd_set_events(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t), t.size,
@@ -92,9 +95,10 @@ def load_window(batch: EventBatch, ctx=None):
         _raise(ctx, rc)
     # read-only arrays: held (so their buffers cannot be freed and reused at
     # the same address); writeable ones: a copy to compare against
-    frozen = all(not a.flags.writeable for a in (x, y, t))
-    ctx._resident = (key, ctx.window_generation,
-                     (x, y, t) if frozen else (x.copy(), y.copy(), t.copy()))
+    if cache:
+        frozen = all(not a.flags.writeable for a in (x, y, t))
+        ctx._resident = (key, ctx.window_generation,
+                         (x, y, t) if frozen else (x.copy(), y.copy(), t.copy()))
     return ctx
 
 

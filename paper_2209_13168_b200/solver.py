@@ -116,7 +116,7 @@ def solve_window(batch: EventBatch, params: SolverParams, ctx=None) -> tuple[Bnb
         raise NoEventsError("no events in batch")
     start = time.perf_counter()
     velocity_domain(batch.tau, params.epsilon)  # ValueError on bad tau / epsilon (geometry.py:63-66)
-    ctx = load_window(batch, ctx)
+    ctx = load_window(batch, ctx, cache=False)
     res, launches = solve_loaded(ctx, params)
     runtime = time.perf_counter() - start
     return (BnbResult(res.nu, res.contrast, res.bound_gap, int(res.iterations), runtime),
