@@ -572,7 +572,8 @@ constexpr unsigned kFar = 0xffffffffu;
 struct TilePoint {
     unsigned code;   // (iy + 8) << 16 | (ix + 8) of the certified cell, or kFar
     int l;           // its local pixel in the tile, or -1
-    int out;         // certainly beyond the left / right / top / bottom edge (bits 0-3)
+    int out;         // certainly beyond the left / right / top / bottom edge (bits 0-3);
+                     // bit 4: the certified cell is in the frame
 };
 
 // The hot path below is written branch-free (selects, non-short-circuit
@@ -635,6 +636,7 @@ __device__ __forceinline__ TilePoint tile_point(float xf, float yf, double t, do
     p.code = sure ? (((unsigned)iy << 16) | (unsigned)ix) : kFar;
     const bool in = sure & (ix >= 8) & (ix < W + 8) & (iy >= 8) & (iy < H + 8);
     p.l = tile_local(v, ix - 8, iy - 8, in);
+    p.out |= in ? 16 : 0;
     return p;
 }
 
@@ -651,13 +653,15 @@ __device__ __forceinline__ bool code_in_frame(unsigned c, int W, int H)
 __device__ __forceinline__ bool tile_pair(const TilePoint &a, const TilePoint &b, int W, int H,
                                           unsigned img, bool on, int &inside)
 {
-    const bool off = (a.out & b.out) != 0;
-    const int dx = (int)(a.code & 0xffffu) - (int)(b.code & 0xffffu);
-    const int dy = (int)(a.code >> 16) - (int)(b.code >> 16);
-    const bool cells = (a.code != kFar) & (b.code != kFar) & (abs(dx) + abs(dy) <= 1);
+    const bool off = (a.out & b.out & 15) != 0;
+    // equal or edge-adjacent cells: codes differ by 0, +-1 or +-2^16 (both
+    // halves of a certified code are in [1, 32000], so no borrow crosses)
+    const unsigned u = a.code - b.code + 65536u;
+    const bool adj = (u == 0u) | (u == 131072u) | (u - 65535u <= 2u);
+    const bool cells = (a.code != kFar) & (b.code != kFar) & adj;
     const bool sure = off | cells;
     const bool mark = on & !off & cells;
-    inside = (mark & code_in_frame(a.code, W, H) & code_in_frame(b.code, W, H)) ? 1 : 0;
+    inside = (mark & ((a.out & b.out & 16) != 0)) ? 1 : 0;
     tile_mark(img, a.l, mark & (a.l >= 0));
     tile_mark(img, b.l, mark & (b.l >= 0) & (b.code != a.code));
     return sure;
