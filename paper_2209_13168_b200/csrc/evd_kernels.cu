@@ -1582,6 +1582,7 @@ struct SpecState {
     unsigned long long marks, exact;
     double mu[kSpecK];
     unsigned long long fiA[kSpecK], fiB[kSpecK];
+    double pwA[kSpecK], pwB[kSpecK];  // mu_lower**2 of each child (the pow2 table)
     double S[kSpecK];
     SpecRes cache[kSpecCache];
     int ncache, cache_head;
@@ -1764,6 +1765,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 Z.mu[s] = ddiv((double)a01.x, (double)M);
                 Z.fiA[s] = a01.y;
                 Z.fiB[s] = a2;
+                Z.pwA[s] = __ldg(a.pow2 + a01.y);  // prefetched for the step
+                Z.pwB[s] = __ldg(a.pow2 + a2);
             }
             if (gb == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + kSpecK * 8)
                 __stcg(&st->sacc[par ^ 1][0][0] + (threadIdx.x - 32), 0ull);
@@ -1815,8 +1818,25 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
 
             // step: finish every slot's contrast and bounds, then replay the
             // reference's pops while their results are known
-            for (int i = threadIdx.x; i < ns * C; i += blockDim.x)
-                scratch[(i / C) * (C + ntop) + (i % C)] = __ldcg(tree.cutval + i);
+            // each slot's child bounds and counts (one thread per slot, in the
+            // CTA's last warp) while the other threads fetch the cut sums
+            __shared__ double s_res[kSpecK][3];
+            __shared__ unsigned long long s_cnt[kSpecK][2];
+            const int sl0 = (int)blockDim.x - 32;
+            if (threadIdx.x >= sl0 && threadIdx.x < sl0 + ns) {
+                const int s = threadIdx.x - sl0;
+                const double Md = (double)M;
+                const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
+                const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
+                const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
+                s_cnt[s][0] = a0 + a23.y;
+                s_cnt[s][1] = a6;
+                s_res[s][1] = dsub(ddiv((double)a45.x, Md), Z.pwA[s]);
+                s_res[s][2] = dsub(ddiv((double)a45.y, Md), Z.pwB[s]);
+            }
+            if ((int)threadIdx.x < sl0)
+                for (int i = threadIdx.x; i < ns * C; i += sl0)
+                    scratch[(i / C) * (C + ntop) + (i % C)] = __ldcg(tree.cutval + i);
             __syncthreads();
             if (C > 1) {
                 const int levels = tree.top_levels;
@@ -1833,21 +1853,11 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 }
             }
             __syncthreads();
-            // each slot's contrast and child bounds, one thread per slot
-            __shared__ double s_res[kSpecK][3];
-            __shared__ unsigned long long s_cnt[kSpecK][2];
+            // each slot's contrast, one thread per slot
             if (threadIdx.x < ns) {
                 const int s = threadIdx.x;
-                const double Md = (double)M;
                 const double Sv = scratch[s * (C + ntop) + (C > 1 ? tree.top_root : 0)];
-                const ulonglong2 a45 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 4));
-                const ulonglong2 a23 = __ldcg(reinterpret_cast<const ulonglong2 *>(sacc[s] + 2));
-                const unsigned long long a0 = __ldcg(sacc[s]), a6 = __ldcg(sacc[s] + 6);
-                s_cnt[s][0] = a0 + a23.y;
-                s_cnt[s][1] = a6;
-                s_res[s][0] = ddiv(dadd(0.0, Sv), Md);  // np.sum(...) / M
-                s_res[s][1] = dsub(ddiv((double)a45.x, Md), __ldg(a.pow2 + Z.fiA[s]));
-                s_res[s][2] = dsub(ddiv((double)a45.y, Md), __ldg(a.pow2 + Z.fiB[s]));
+                s_res[s][0] = ddiv(dadd(0.0, Sv), (double)M);  // np.sum(...) / M
             }
             __syncthreads();
             if (threadIdx.x == 0) {
