@@ -1864,8 +1864,10 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 Z.rounds++;
                 for (int s = 0; s < ns; s++) {
                     Z.marks += s_cnt[s][0];
+#ifndef EVD_STEP_PROBE
                     if (tr && gb == 0 && it < a.trace_iters)  // round's marks, slots
                         a.trace[1 + kTraceSlots * it + kTrMarks] += (long long)s_cnt[s][0];
+#endif
                     Z.exact += s_cnt[s][1];
                     const double Cs = s_res[s][0], cbA = s_res[s][1], cbB = s_res[s][2];
                     if (s == 0 && mode == kModeRoot) {
@@ -1885,114 +1887,98 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 if (Z.status == kStatusSpecOverflow) Z.done = 1;
             }
             __syncthreads();
+#ifdef EVD_STEP_PROBE
+            if (tr && gb == 0) trace_point(a, it, kTrMarks);
+#endif
             if (threadIdx.x < 32 && !Z.done) {
-                // warp 0: the pop loop (lane 0 runs the serial parts)
+                // warp 0: the pop loop.  The BnB state lives in registers,
+                // identical in every lane (each lane computes the same values
+                // from the same shared-memory reads); lane 0 writes the
+                // frontier entries and, at the end, the state back to Z.
                 SpecSlot node = Z.slot[0];
                 bool root = mode == kModeRoot;
                 int stop = 0, next_uncached = 0;
-                while (true) {
-                    if (lane == 0) {
-                        if (root) {  // solver.py:92-98
-                            Z.c_hat = Z.S[0];
-                            Z.nu_hat = node.c;
-                            Z.point_evals++;
-                            Z.bound_evals++;
-                            if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
-                                Z.status = kStatusSpecOverflow;
-                                stop = 1;
-                            } else {
-                                frs[Z.fr_n++] = FrontierEntry{Z.mu[0], Z.next_counter++, node.lo,
-                                                              node.hi};
-                            }
-                        } else {  // solver.py:109-119
-                            const SpecRes &r = Z.cache[Z.cur];
-                            Z.point_evals++;
-                            if (r.C >= Z.c_hat) {
-                                Z.nu_hat = node.c;
-                                Z.c_hat = r.C;
-                            }
-                            Z.bound_evals += 2;
-                            const double cbA = r.cbA, cbB = r.cbB;
-                            if (cbA >= Z.c_hat) {
-                                if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
-                                    Z.status = kStatusSpecOverflow;
-                                    stop = 1;
-                                } else {
-                                    frs[Z.fr_n++] = FrontierEntry{cbA, Z.next_counter++, node.lo,
-                                                                  node.c};
-                                }
-                            }
-                            if (!stop && cbB >= Z.c_hat) {
-                                if (Z.fr_n >= kSpecFr || Z.fr_n >= a.fr_cap) {
-                                    Z.status = kStatusSpecOverflow;
-                                    stop = 1;
-                                } else {
-                                    frs[Z.fr_n++] = FrontierEntry{cbB, Z.next_counter++, node.c,
-                                                                  node.hi};
-                                }
-                            }
-                            if (!stop && Z.iterations >= a.max_iter) {
-                                Z.status = kStatusIterLimit;
-                                stop = 1;
-                            }
-                        }
-                        if (Z.fr_n > Z.max_fr) Z.max_fr = Z.fr_n;
-                        if (!stop && Z.fr_n == 0) stop = 1;  // every interval pruned
+                double c_hat = Z.c_hat, nu_hat = Z.nu_hat, bound_gap = Z.bound_gap;
+                int fr_n = (int)Z.fr_n, cur = Z.cur, status = Z.status;
+                long long next_counter = Z.next_counter, iterations = Z.iterations;
+                long long point_evals = Z.point_evals, bound_evals = Z.bound_evals;
+                long long max_fr = Z.max_fr;
+                auto push = [&](double bound, double lo, double hi) {
+                    if (fr_n >= kSpecFr || fr_n >= a.fr_cap) {
+                        status = kStatusSpecOverflow;
+                        stop = 1;
+                    } else {
+                        if (lane == 0) frs[fr_n] = FrontierEntry{bound, next_counter, lo, hi};
+                        fr_n++;
+                        next_counter++;
                     }
-                    stop = __shfl_sync(0xffffffffu, stop, 0);
+                };
+                while (true) {
+                    if (root) {  // solver.py:92-98
+                        c_hat = Z.S[0];
+                        nu_hat = node.c;
+                        point_evals++;
+                        bound_evals++;
+                        push(Z.mu[0], node.lo, node.hi);
+                    } else {  // solver.py:109-119
+                        const SpecRes &r = Z.cache[cur];
+                        point_evals++;
+                        if (r.C >= c_hat) {
+                            nu_hat = node.c;
+                            c_hat = r.C;
+                        }
+                        bound_evals += 2;
+                        const double cbA = r.cbA, cbB = r.cbB;
+                        if (cbA >= c_hat) push(cbA, node.lo, node.c);
+                        if (!stop && cbB >= c_hat) push(cbB, node.c, node.hi);
+                        if (!stop && iterations >= a.max_iter) {
+                            status = kStatusIterLimit;
+                            stop = 1;
+                        }
+                    }
+                    if (fr_n > max_fr) max_fr = fr_n;
+                    if (!stop && fr_n == 0) stop = 1;  // every interval pruned
                     if (stop) break;
                     __syncwarp();
-                    const long long bi = spec_argmax(frs, Z.fr_n, [](const FrontierEntry &) {
+                    const long long bi = spec_argmax(frs, fr_n, [](const FrontierEntry &) {
                         return false;
                     });
                     const FrontierEntry top = frs[bi];
                     const int hit = spec_find(Z, top.counter & ~kSpecFlag);
                     __syncwarp();
-                    if (lane == 0) {
-                        frs[bi] = frs[Z.fr_n - 1];  // swap-remove
-                        Z.fr_n--;
-                        Z.iterations++;
-                        const double gap = dsub(top.bound, Z.c_hat);  // solver.py:105-108
-                        if (gap <= a.gamma || dsub(top.hi, top.lo) < a.min_width) {
-                            Z.bound_gap = (0.0 > gap) ? 0.0 : gap;
-                            stop = 1;
-                        } else {
-                            spec_set_slot(a, node, top);
-                            if (hit >= 0) Z.cur = hit;
-                            else next_uncached = 1;
-                        }
+                    if (lane == 0) frs[bi] = frs[fr_n - 1];  // swap-remove
+                    fr_n--;
+                    iterations++;
+                    const double gap = dsub(top.bound, c_hat);  // solver.py:105-108
+                    if (gap <= a.gamma || dsub(top.hi, top.lo) < a.min_width) {
+                        bound_gap = (0.0 > gap) ? 0.0 : gap;
+                        stop = 1;
+                        break;
                     }
-                    stop = __shfl_sync(0xffffffffu, stop, 0);
-                    next_uncached = __shfl_sync(0xffffffffu, next_uncached, 0);
-                    if (stop) break;
-                    // the popped node's interval, for the next iteration / round
-                    node.lo = __shfl_sync(0xffffffffu, node.lo, 0);
-                    node.hi = __shfl_sync(0xffffffffu, node.hi, 0);
-                    node.c = __shfl_sync(0xffffffffu, node.c, 0);
-                    node.den_lo = __shfl_sync(0xffffffffu, node.den_lo, 0);
-                    node.den_c = __shfl_sync(0xffffffffu, node.den_c, 0);
-                    node.den_hi = __shfl_sync(0xffffffffu, node.den_hi, 0);
-                    node.counter = __shfl_sync(0xffffffffu, node.counter, 0);
+                    spec_set_slot(a, node, top);
                     root = false;
-                    if (next_uncached) break;
+                    __syncwarp();
+                    if (hit >= 0) {
+                        cur = hit;
+                    } else {
+                        next_uncached = 1;
+                        break;
+                    }
                 }
-                if (stop) {
-                    if (lane == 0) Z.done = 1;
-                } else {
+#ifdef EVD_STEP_PROBE
+                if (tr && gb == 0) trace_point(a, it, kTrExact);
+#endif
+                __syncwarp();
+                int nslot = 1;
+                if (!stop) {
                     // next round: the popped node, then the best narrow uncached
                     // entries of the frontier
-                    if (lane == 0) {
-                        Z.slot[0] = node;
-                        Z.nslot = 1;
-                        Z.mode = kModeNode;
-                    }
-                    __syncwarp();
                     for (int s = 1; s < K; s++) {
-                        const long long bi = spec_argmax(frs, Z.fr_n, [&](const FrontierEntry &e) {
+                        const long long bi = spec_argmax(frs, fr_n, [&](const FrontierEntry &e) {
                             if (dsub(e.hi, e.lo) > kSpecWidth) return true;
                             // never evaluated by the reference: popping it ends
                             // the search (solver.py:106-108; c_hat only grows)
-                            if (dsub(e.bound, Z.c_hat) <= a.gamma ||
+                            if (dsub(e.bound, c_hat) <= a.gamma ||
                                 dsub(e.hi, e.lo) < a.min_width)
                                 return true;
                             // evaluated or scheduled already (its result is
@@ -2001,20 +1987,42 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                         });
                         if (bi < 0) break;
                         if (lane == 0) {
-                            spec_set_slot(a, Z.slot[Z.nslot], frs[bi]);
+                            spec_set_slot(a, Z.slot[nslot], frs[bi]);
                             frs[bi].counter |= kSpecFlag;
-                            Z.nslot++;
                         }
+                        nslot++;
                         __syncwarp();
                     }
-                    if (lane == 0) Z.parity = par ^ 1;
+                }
+                if (lane == 0) {
+                    Z.c_hat = c_hat;
+                    Z.nu_hat = nu_hat;
+                    Z.bound_gap = bound_gap;
+                    Z.fr_n = fr_n;
+                    Z.cur = cur;
+                    Z.status = status;
+                    Z.next_counter = next_counter;
+                    Z.iterations = iterations;
+                    Z.point_evals = point_evals;
+                    Z.bound_evals = bound_evals;
+                    Z.max_fr = max_fr;
+                    if (stop) {
+                        Z.done = 1;
+                    } else {
+                        Z.slot[0] = node;
+                        Z.nslot = nslot;
+                        Z.mode = kModeNode;
+                        Z.parity = par ^ 1;
+                    }
                 }
             }
             __syncthreads();
             if (tr && gb == 0) {
                 trace_point(a, it, kTrB0Step1);
+#ifndef EVD_STEP_PROBE
                 if (threadIdx.x == 0 && it < a.trace_iters)
                     a.trace[1 + kTraceSlots * it + kTrExact] = ns;  // slots this round
+#endif
             }
         }
         // speculative slots' point images are summed (and cleared) every round;
