@@ -117,13 +117,17 @@ int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k
  *                            "frontier_image_budget" bytes per launch, larger
  *                            k in chunks), filtered warp + exact fallback;
  *  EVD_FRONTIER_GLOBAL_EXACT the same with exact warps only;
- *  EVD_FRONTIER_AUTO         tiles when they apply, else global (default).
+ *  EVD_FRONTIER_PER_INTERVAL one evd_bound_images pass per interval (lane =
+ *                            event: best for a few, wide intervals);
+ *  EVD_FRONTIER_AUTO         per-interval up to 32 intervals, else tiles
+ *                            when they apply, else global (default).
  * Every path returns identical integers. */
 enum {
     EVD_FRONTIER_AUTO = 0,
     EVD_FRONTIER_TILES = 1,
     EVD_FRONTIER_GLOBAL = 2,
-    EVD_FRONTIER_GLOBAL_EXACT = 3
+    EVD_FRONTIER_GLOBAL_EXACT = 3,
+    EVD_FRONTIER_PER_INTERVAL = 4
 };
 int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
                       uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks);

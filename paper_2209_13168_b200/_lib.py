@@ -21,6 +21,7 @@ EVD_OK, EVD_ERR_CUDA, EVD_ERR_ARG, EVD_ERR_NO_EVENTS = 0, 1, 2, 3
 EVD_ERR_CHEIRALITY, EVD_ERR_ITER_LIMIT, EVD_ERR_STATE = 4, 5, 6
 EVD_ERR_FORMAT, EVD_ERR_VALIDATION = 7, 8
 FRONTIER_AUTO, FRONTIER_TILES, FRONTIER_GLOBAL, FRONTIER_GLOBAL_EXACT = 0, 1, 2, 3
+FRONTIER_PER_INTERVAL = 4
 
 # every symbol include/evd.h declares (checked by tests/test_abi.py)
 SYMBOLS = (

@@ -802,6 +802,8 @@ int evd_bound_images(evd_ctx *ctx, const double *lo, const double *hi, int32_t k
     return EVD_OK;
 }
 
+constexpr int kFrontierSmallK = 32;  // auto: per-interval passes up to this many intervals
+
 int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t k,
                       uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks)
 {
@@ -822,6 +824,16 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
         host[(size_t)k + j] = hi[j];
         nonpositive = nonpositive && hi[j] <= 0.0;
         if (j > 0 && lo[j] != hi[j - 1]) contig = false;
+    }
+    // A few intervals: one k_bound_image pass each (lane = event) beats the
+    // frontier kernels (lane = interval, mostly idle lanes at small k): cfg 5
+    // root 11.6 vs 21.5 ms, 32 intervals of width 1/16 30.7 vs 45.7 ms
+    // (tools/probe_small_k.py)
+    if (ctx->frontier_path == EVD_FRONTIER_PER_INTERVAL ||
+        (ctx->frontier_path == EVD_FRONTIER_AUTO && k <= kFrontierSmallK)) {
+        rc = evd_bound_images(ctx, lo, hi, k, s_bar, fully_inside, marks, nullptr);
+        if (!rc) ctx->last_frontier_path = EVD_FRONTIER_PER_INTERVAL;
+        return rc;
     }
     CU(cudaSetDevice(ctx->device));
     CU(ctx->fargs.ensure(4 * (size_t)k));
@@ -886,7 +898,7 @@ int evd_set_option(evd_ctx *ctx, const char *name, int64_t value)
     if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
     if (!name) return fail(ctx, EVD_ERR_ARG, "option name is NULL");
     if (!strcmp(name, "frontier_path")) {
-        if (value < EVD_FRONTIER_AUTO || value > EVD_FRONTIER_GLOBAL_EXACT)
+        if (value < EVD_FRONTIER_AUTO || value > EVD_FRONTIER_PER_INTERVAL)
             return fail(ctx, EVD_ERR_ARG, "frontier_path %lld out of range", (long long)value);
         ctx->frontier_path = (int)value;
         return EVD_OK;

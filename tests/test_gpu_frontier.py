@@ -156,12 +156,14 @@ def test_tiled_frontier_landing_windows(frontier_path):
 
 def test_tiled_frontier_fallbacks(frontier_path):
     """Auto takes the global path where tiles do not apply (nu > 0, non-finite
-    events); forcing tiles there fails loudly."""
+    events) and more than 32 intervals are asked for; forcing tiles there
+    fails loudly."""
     from paper_2209_13168_b200 import _lib
     ctx = frontier_path
     r = np.random.default_rng(3)
     b = synth.random_window(r, 64, 48, 2000)
-    lo, hi = np.array([-0.5, -0.1, 0.0]), np.array([-0.1, 0.2, 0.3])   # nu > 0
+    edges = np.linspace(-0.5, 0.3, 41)
+    lo, hi = edges[:-1], edges[1:]   # 40 intervals, the last ones with nu > 0
     a = con.frontier_terms(b, lo, hi, ctx=ctx)
     assert ctx.frontier_info()["last_path"] == _lib.FRONTIER_GLOBAL
     c = con.bound_terms_many(b, lo, hi, ctx=ctx)
@@ -175,10 +177,33 @@ def test_tiled_frontier_fallbacks(frontier_path):
     with pytest.raises(_lib.EvdError):
         con.frontier_terms(bn, [-0.5], [-0.1], ctx=ctx)
     ctx.set_option("frontier_path", _lib.FRONTIER_AUTO)
-    a = con.frontier_terms(bn, [-0.5, -1.0], [-0.1, -0.5], ctx=ctx)
+    edges = np.linspace(-1.0, -0.1, 41)
+    a = con.frontier_terms(bn, edges[:-1], edges[1:], ctx=ctx)
     assert ctx.frontier_info()["last_path"] == _lib.FRONTIER_GLOBAL
-    c = con.bound_terms_many(bn, [-0.5, -1.0], [-0.1, -0.5], ctx=ctx)
+    c = con.bound_terms_many(bn, edges[:-1], edges[1:], ctx=ctx)
     assert all(np.array_equal(u, v) for u, v in zip(a, c[:3]))
+
+
+@pytest.mark.parametrize("k", [1, 5, 32, 33])
+def test_frontier_small_k_per_interval(frontier_path, k):
+    """Auto evaluates up to 32 intervals one k_bound_image pass each and more
+    on the tiled kernel; both give the integers of the tiled and global paths."""
+    from paper_2209_13168_b200 import _lib
+    ctx = frontier_path
+    r = np.random.default_rng(40 + k)
+    b = synth.random_window(r, 96, 64, 5000)
+    edges = np.sort(r.uniform(-1.5, 0.0, k + 1))
+    lo, hi = edges[:-1], edges[1:]
+    auto = con.frontier_terms(b, lo, hi, ctx=ctx)
+    want = _lib.FRONTIER_PER_INTERVAL if k <= 32 else _lib.FRONTIER_TILES
+    assert ctx.frontier_info()["last_path"] == want
+    for code in (_lib.FRONTIER_TILES, _lib.FRONTIER_GLOBAL, _lib.FRONTIER_PER_INTERVAL):
+        ctx.set_option("frontier_path", code)
+        got = con.frontier_terms(b, lo, hi, ctx=ctx)
+        assert ctx.frontier_info()["last_path"] == code
+        assert all(np.array_equal(u, v) for u, v in zip(auto, got))
+    with pytest.raises(_lib.EvdError):
+        ctx.set_option("frontier_path", 5)
 
 
 def test_cfg3_frontier_sample_vs_oracle():

@@ -2,7 +2,7 @@
 the 4096 depth-12 leaves of the root bisection in one evd_eval_frontier call).
 
 python tools/bench_frontier.py [reps] [path]   -> one JSON line
-path: auto (default) | tiles | global | global_exact (evd_set_option "frontier_path")
+path: auto (default) | tiles | global | global_exact | per_interval (evd_set_option "frontier_path")
 """
 
 import json
@@ -26,7 +26,8 @@ def main():
     lo, hi = fr.uniform_frontier(velocity_domain(b.tau), 12)
     ctx = _lib.context()
     path = sys.argv[2] if len(sys.argv) > 2 else "auto"
-    ctx.set_option("frontier_path", {"auto": 0, "tiles": 1, "global": 2, "global_exact": 3}[path])
+    ctx.set_option("frontier_path", {"auto": 0, "tiles": 1, "global": 2, "global_exact": 3,
+                                     "per_interval": 4}[path])
     stream = torch.cuda.Stream()  # explicit: handle 0 would mean the context's own stream
     torch.cuda.set_stream(stream)
     ctx.lib.evd_set_stream(ctx.h, _lib._vp(stream.cuda_stream))
