@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -122,6 +123,15 @@ struct evd_ctx {
     unsigned char *stage = nullptr;
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    // evd_solve_stream from host arrays: the raw stream is uploaded on a copy
+    // stream through a ring of pinned chunk slots while the solve runs
+    bool stream_overlap = true;               // evd_set_option("stream_overlap")
+    long long feed_chunk = 1ll << 16;         // events per chunk (option "stream_chunk")
+    cudaStream_t copy = nullptr;
+    cudaEvent_t feed_ev[8] = {};
+    cudaEvent_t feed_start = nullptr;
+    DevBuf<unsigned long long> feedw;         // [0] raw events delivered, [1] stall flag
+    DevBuf<long long> feedb;                  // per window: raw lo, count, unpadded offsets
 };
 
 namespace {
@@ -488,6 +498,12 @@ void evd_destroy(evd_ctx *ctx)
     tp.top.release();
     tp.cutval.release();
     tiles_free(ctx->tiles);
+    ctx->feedw.release();
+    ctx->feedb.release();
+    for (cudaEvent_t e : ctx->feed_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->feed_start) cudaEventDestroy(ctx->feed_start);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->stage) cudaFreeHost(ctx->stage);
     for (cudaEvent_t e : ctx->stage_ev)
         if (e) cudaEventDestroy(e);
@@ -903,6 +919,17 @@ int evd_set_option(evd_ctx *ctx, const char *name, int64_t value)
         ctx->frontier_path = (int)value;
         return EVD_OK;
     }
+    if (!strcmp(name, "stream_overlap")) {
+        if (value != 0 && value != 1) return fail(ctx, EVD_ERR_ARG, "stream_overlap must be 0 or 1");
+        ctx->stream_overlap = value != 0;
+        return EVD_OK;
+    }
+    if (!strcmp(name, "stream_chunk")) {
+        if (value < 1024 || value > (1ll << 18))
+            return fail(ctx, EVD_ERR_ARG, "stream_chunk must be in [1024, 262144] events");
+        ctx->feed_chunk = value;
+        return EVD_OK;
+    }
     if (!strcmp(name, "frontier_image_budget")) {
         if (value < 1) return fail(ctx, EVD_ERR_ARG, "frontier_image_budget must be positive");
         ctx->frontier_budget = value;
@@ -984,9 +1011,19 @@ constexpr long long kSpecMaxEvents = 2000000;
 constexpr long long kSmallWindow = 32768;     // 384-thread CTAs below this
 constexpr long long kLargeWindow = 250000;    // 768-thread CTAs from this on
 
+// Overlapped upload of a host stream into a running solve (evd_solve_stream):
+// the device arrays k_solve / k_solve_spec gather from, and the host loop that
+// feeds them (issued once, right after the first launch).
+struct StreamFeed {
+    const long long *s_lo, *counts;   // device, per window
+    const long long *h_counts;        // host copy of counts
+    long long k0;
+    std::function<int()> upload;
+};
+
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
-                       float *ms_out)
+                       float *ms_out, StreamFeed *feed = nullptr)
 {
     int rc;
     if (!(params->gamma > 0.0)) return fail(ctx, EVD_ERR_ARG, "gamma must be positive");
@@ -1004,7 +1041,8 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     groups = std::max(1, std::min(groups, ctx->solve_blocks));
     const int GB = ctx->solve_blocks / groups;
     long long max_n = 0;
-    for (int w = 0; w < n_windows; w++) max_n = std::max(max_n, off[w + 1] - off[w]);
+    for (int w = 0; w < n_windows; w++)
+        max_n = std::max(max_n, feed ? feed->h_counts[w] : off[w + 1] - off[w]);
     // speculative rounds (k_solve_spec) unless EVD_SPEC_K=1 or the timeline
     // trace is on (k_solve has the probes)
     // (on the whole grid: 3 slots measured best with 384-thread CTAs, 4 above,
@@ -1090,12 +1128,37 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         a.filter = (max_n >= kFilterMinEvents) ? 1 : 0;
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         a.spec_k = spec_k;
+        if (feed) {
+            a.sx = ctx->sx.p;
+            a.sy = ctx->sy.p;
+            a.stt = ctx->st.p;
+            a.s_lo = feed->s_lo;
+            a.counts = feed->counts;
+            a.ready = ctx->feedw.p;
+            a.stall = reinterpret_cast<unsigned int *>(ctx->feedw.p + 1);
+            a.gx = ctx->xc.p;
+            a.gy = ctx->yc.p;
+            a.gt = ctx->t.p;
+            a.k0 = feed->k0;
+        }
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
         CU((spec_k > 1 || getenv("EVD_SPEC_FORCE"))
                ? launch_solve_spec(a, groups * GB, threads, ctx->stream)
                : launch_solve(a, groups * GB, threads, ctx->stream));
         LAUNCHED(1);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
+        if (feed && feed->upload) {
+            // the solve waits on the chunks: feed them now (host copies into
+            // pinned slots, device copies on ctx->copy)
+            const int urc = feed->upload();
+            feed->upload = nullptr;
+            if (urc) {
+                // release the waiting groups (their windows are garbage), then report
+                cudaMemsetAsync(ctx->feedw.p, 0xff, sizeof(unsigned long long), ctx->copy);
+                cudaStreamSynchronize(ctx->stream);
+                return urc;
+            }
+        }
         std::vector<WindowResult> got(n_windows);
         CU(cudaMemcpyAsync(got.data(), ctx->wres.p, n_windows * sizeof(WindowResult),
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -1103,6 +1166,13 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         total_ms += ms;
+        if (feed) {
+            unsigned long long stall = 0;
+            CU(cudaMemcpyAsync(&stall, ctx->feedw.p + 1, sizeof stall, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            if (stall) return fail(ctx, EVD_ERR_CUDA, "stream upload did not arrive in time");
+        }
         bool again = false, overflow = false;
         for (int w : todo) {
             out[w] = got[w];
@@ -1160,7 +1230,7 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
 // evd_solve_windows and evd_solve_stream).
 static int solve_offsets(evd_ctx *ctx, const long long *offsets, int n_windows, int groups,
                          const evd_solve_params *params, evd_window_result *results,
-                         double *device_ms)
+                         double *device_ms, StreamFeed *feed = nullptr)
 {
     int rc;
     if (groups <= 0) {
@@ -1168,6 +1238,10 @@ static int solve_offsets(evd_ctx *ctx, const long long *offsets, int n_windows, 
         // (cfg4, 2000 windows of ~20k events: 74 groups of 2 CTAs measured best;
         // smaller groups trade the grid barrier for per-thread event loops)
         long long tot = offsets[n_windows] - offsets[0];
+        if (feed) {
+            tot = 0;
+            for (int w = 0; w < n_windows; w++) tot += feed->h_counts[w];
+        }
         const double avg = (double)tot / n_windows;
         if (!ctx->solve_blocks) ctx->solve_blocks = solve_grid_blocks(ctx->device);
         const int per = std::max(1, (int)std::ceil(avg / (20.0 * solve_block_threads())));
@@ -1175,7 +1249,7 @@ static int solve_offsets(evd_ctx *ctx, const long long *offsets, int n_windows, 
     }
     std::vector<WindowResult> out;
     float ms = 0.f;
-    if ((rc = run_windows(ctx, offsets, n_windows, groups, params, out, &ms))) return rc;
+    if ((rc = run_windows(ctx, offsets, n_windows, groups, params, out, &ms, feed))) return rc;
     for (int w = 0; w < n_windows; w++) {
         evd_window_result &r = results[w];
         r.nu = out[w].nu;
@@ -1281,6 +1355,145 @@ static int solve_resident_stream(evd_ctx *ctx, double tau, int groups,
     return solve_offsets(ctx, o.data(), nw, groups, params, results, device_ms);
 }
 
+// lower_bound of v in t[0, n) with k_window_bounds' loop (the same result on
+// any input, sorted or not)
+static long long host_lower_bound(const double *t, long long n, double v)
+{
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (t[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// evd_solve_stream from host arrays: the windows' bounds come from the host
+// copy of t, the solve is launched at once, and the raw stream follows in
+// chunks on ctx->copy (host memcpy into a ring of pinned slots, then H2D);
+// each window's group starts when its events have arrived.  The solve layout
+// pads every window to 16 events; once the solve is done the resident window
+// set is re-gathered unpadded (the evd_set_events contract).
+static int solve_stream_overlapped(evd_ctx *ctx, const double *x, const double *y,
+                                   const double *t, long long n, bool pinned, double tau,
+                                   int groups,
+                                   const evd_solve_params *params, evd_window_result *results,
+                                   int capacity, int32_t *n_windows, int64_t *k0_out,
+                                   double *device_ms)
+{
+    // events.py:341-342 on the host copy of t
+    const double f0 = std::floor(t[0] / tau), f1 = std::floor(t[n - 1] / tau);
+    if (!(f0 >= 0.0) || !(f1 >= f0) || f1 - f0 >= 2147483647.0)
+        return fail(ctx, EVD_ERR_ARG, "timestamps must be sorted, non-negative and finite");
+    const long long k0 = (long long)f0;
+    const int nw = (int)((long long)f1 - k0 + 1);
+    *n_windows = nw;
+    *k0_out = k0;
+    if (!results || capacity < nw)
+        return fail(ctx, EVD_ERR_ARG, "stream spans %d windows, results hold %d", nw, capacity);
+    std::vector<long long> lo(nw), cnt(nw), pad(nw + 1), o(nw + 1);
+    pad[0] = o[0] = 0;
+    for (int w = 0; w < nw; w++) {
+        const double start = (double)(k0 + w) * tau;
+        lo[w] = host_lower_bound(t, n, start);
+        cnt[w] = std::max(0LL, host_lower_bound(t, n, start + tau) - lo[w]);
+        o[w + 1] = o[w] + cnt[w];
+        pad[w + 1] = pad[w] + (cnt[w] + 15) / 16 * 16;
+    }
+    const long long total = o[nw];
+    CU(ctx->xc.ensure(std::max(pad[nw], 1LL)));
+    CU(ctx->yc.ensure(std::max(pad[nw], 1LL)));
+    CU(ctx->t.ensure(std::max(pad[nw], 1LL)));
+    CU(ctx->feedw.ensure(2));
+    CU(ctx->feedb.ensure(3 * (size_t)nw + 1));
+    long long *d_lo = ctx->feedb.p, *d_cnt = d_lo + nw, *d_off = d_cnt + nw;
+    if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    if (!ctx->feed_start) {
+        CU(cudaEventCreateWithFlags(&ctx->feed_start, cudaEventDisableTiming));
+        for (cudaEvent_t &e : ctx->feed_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const size_t half = 16u << 20;
+    if (!ctx->stage) {
+        CU(cudaHostAlloc(&ctx->stage, 2 * half, cudaHostAllocDefault));
+        ctx->stage_bytes = 2 * half;
+        CU(cudaEventCreateWithFlags(&ctx->stage_ev[0], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ctx->stage_ev[1], cudaEventDisableTiming));
+    }
+    CU(cudaMemsetAsync(ctx->feedw.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    CU(cudaMemcpyAsync(d_lo, lo.data(), nw * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(d_cnt, cnt.data(), nw * sizeof(long long), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(d_off, o.data(), (nw + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    // the copies start after everything queued so far (earlier readers of sx / sy / st)
+    CU(cudaEventRecord(ctx->feed_start, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->copy, ctx->feed_start, 0));
+    ctx->W = ctx->sW;
+    ctx->H = ctx->sH;
+    ctx->tau = tau;
+    ctx->gen++;
+    ctx->n = 0;  // the resident window set is rebuilt below
+    const long long S = std::min<long long>(ctx->feed_chunk, (long long)(2 * half / 8 / 32));
+    const int slots = 8;
+    const size_t slot_bytes = (size_t)S * 3 * sizeof(double) + 64;
+    StreamFeed feed{d_lo, d_cnt, cnt.data(), k0, nullptr};
+    feed.upload = [&]() -> int {
+        for (long long c0 = 0, c = 0; c0 < n; c0 += S, c++) {
+            const int sl = (int)(c % slots);
+            if (c >= slots) CU(cudaEventSynchronize(ctx->feed_ev[sl]));  // slot free again
+            const long long m = std::min(S, n - c0);
+            double *px = reinterpret_cast<double *>(ctx->stage + sl * slot_bytes);
+            double *py = px + S, *pt = py + S;
+            unsigned long long *val = reinterpret_cast<unsigned long long *>(pt + S);
+            if (pinned) {  // page-locked already: DMA straight from the caller's arrays
+                px = const_cast<double *>(x + c0);
+                py = const_cast<double *>(y + c0);
+                pt = const_cast<double *>(t + c0);
+            } else {
+                memcpy(px, x + c0, m * sizeof(double));
+                memcpy(py, y + c0, m * sizeof(double));
+                memcpy(pt, t + c0, m * sizeof(double));
+            }
+            *val = (unsigned long long)(c0 + m);
+            CU(cudaMemcpyAsync(ctx->sx.p + c0, px, m * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx->copy));
+            CU(cudaMemcpyAsync(ctx->sy.p + c0, py, m * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx->copy));
+            CU(cudaMemcpyAsync(ctx->st.p + c0, pt, m * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx->copy));
+            CU(cudaMemcpyAsync(ctx->feedw.p, val, sizeof *val, cudaMemcpyHostToDevice, ctx->copy));
+            CU(cudaEventRecord(ctx->feed_ev[sl], ctx->copy));
+        }
+        return EVD_OK;
+    };
+    int rc = EVD_OK;
+    if (total == 0) {  // every window empty: nothing to solve, the stream still goes up
+        if ((rc = feed.upload())) return rc;
+        for (int w = 0; w < nw; w++) {
+            results[w] = evd_window_result{};
+            results[w].status = EVD_ERR_NO_EVENTS;
+        }
+        if (device_ms) *device_ms = 0.0;
+    } else if ((rc = solve_offsets(ctx, pad.data(), nw, groups, params, results, device_ms,
+                                   &feed))) {
+        CU(cudaStreamSynchronize(ctx->copy));
+        return rc;
+    }
+    // the copy stream is done (every window waited for its chunk, or the empty
+    // case): resident window set = the windows concatenated, unpadded
+    CU(cudaStreamSynchronize(ctx->copy));
+    if (total > 0) {
+        launch_gather_windows(ctx->sx.p, ctx->sy.p, ctx->st.p, d_lo, d_off, nw, k0, total, tau,
+                              ctx->sW / 2.0, ctx->sH / 2.0, ctx->xc.p, ctx->yc.p, ctx->t.p,
+                              ctx->stream);
+        LAUNCHED(1);
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->n = total;
+    ctx->gen++;
+    return EVD_OK;
+}
+
 int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
                      int32_t width, int32_t height, double tau, int32_t groups,
                      const evd_solve_params *params, evd_window_result *results,
@@ -1296,6 +1509,25 @@ int evd_solve_stream(evd_ctx *ctx, const double *x, const double *y, const doubl
     CU(ctx->sx.ensure(std::max(n, (int64_t)1)));
     CU(ctx->sy.ensure(std::max(n, (int64_t)1)));
     CU(ctx->st.ensure(std::max(n, (int64_t)1)));
+    // all three arrays in host memory: overlap their upload with the solve
+    bool host = false, pinned = false;
+    if (n > 0 && ctx->stream_overlap) {
+        host = pinned = true;
+        for (const double *q : {x, y, t}) {
+            cudaPointerAttributes at{};
+            CU(cudaPointerGetAttributes(&at, q));
+            host = host && (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered);
+            pinned = pinned && at.type == cudaMemoryTypeHost;
+        }
+    }
+    if (host) {
+        ctx->sn = n;
+        ctx->sW = width;
+        ctx->sH = height;
+        ctx->s_has_p = false;
+        return solve_stream_overlapped(ctx, x, y, t, n, pinned, tau, groups, params, results,
+                                       capacity, n_windows, k0_out, device_ms);
+    }
     if (n > 0) {
         CU(cudaMemcpyAsync(ctx->sx.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->stream));
         CU(cudaMemcpyAsync(ctx->sy.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->stream));

@@ -90,7 +90,20 @@ struct SolveArgs {
     long long *btrace;            // [kBTraceIters][group_blocks][kBTraceSlots] (or null)
     int filter;                   // use the filtered (approximate-then-exact) event path
     int spec_k;                   // k_solve_spec: evaluations per round (1..kSpecK)
+    // Overlapped stream upload (evd_solve_stream from host arrays; sx null:
+    // the windows are already gathered).  The raw stream arrives in chunks on
+    // a copy stream while the solve runs; *ready = raw events on the device.
+    // Window w's group waits for ready >= s_lo[w] + counts[w], then gathers
+    // the window into xc / yc / t at offsets[w] (offsets padded to 16 events:
+    // no cache line holds two windows) before its first node.
+    const double *sx, *sy, *stt;  // raw x, y, t
+    const long long *s_lo, *counts;
+    const unsigned long long *ready;
+    double *gx, *gy, *gt;         // xc / yc / t, writable
+    long long k0;
+    unsigned int *stall;          // set when an upload never arrived (the window is garbage)
 };
+constexpr long long kUploadTimeoutNs = 20000000000ll;  // 20 s
 
 constexpr int kBTraceIters = 128;
 constexpr int kBTraceSlots = 20;

@@ -831,6 +831,43 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     __syncthreads();
 }
 
+// Overlapped stream upload: the group of window w waits (thread 0 of each
+// CTA) until the copy stream has delivered the window's raw events, then
+// gathers them into the solve layout with k_gather_windows' arithmetic
+// (centred x, y; t - start capped at tau, events.py:348).  The raw stream is
+// read through L2 (__ldcg: written by the copy engine during this kernel);
+// the gathered region is read by the group only after the grid barrier that
+// follows, and no other window shares its cache lines (padded offsets).
+__device__ __noinline__ void gather_window(const SolveArgs &a, int w, long long off, long long n,
+                                           int gb, int GB)
+{
+    const long long lo = a.s_lo[w];
+    if (threadIdx.x == 0) {
+        const unsigned long long need = (unsigned long long)(lo + n);
+        const long long t0 = globaltimer();
+        unsigned long long v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.ready) : "memory");
+            if (v >= need) break;
+            if (globaltimer() - t0 > kUploadTimeoutNs) {
+                atomicExch(a.stall, 1u);
+                break;
+            }
+            __nanosleep(500);
+        }
+    }
+    __syncthreads();
+    const double start = dmul((double)(a.k0 + w), a.tau);
+    for (long long j = (long long)gb * blockDim.x + threadIdx.x; j < n;
+         j += (long long)GB * blockDim.x) {
+        const long long i = lo + j;
+        a.gx[off + j] = dsub(__ldcg(a.sx + i), a.cx);
+        a.gy[off + j] = dsub(__ldcg(a.sy + i), a.cy);
+        const double d = dsub(__ldcg(a.stt + i), start);
+        a.gt[off + j] = d < a.tau ? d : a.tau;
+    }
+}
+
 // One node's events on the exact path (k_solve's event phase; also timed
 // alone by k_event_probe): every event, three warps (lo, centre, hi); point
 // image at the centre, segment images of both children (root: of the root),
@@ -1277,11 +1314,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
     if (tracer && gb == 0) trace_point(a, 0, -1);
 
     for (int w = grp; w < a.n_windows; w += a.groups) {
-        const long long off = a.offsets[w], n = a.offsets[w + 1] - off;
+        const long long off = a.offsets[w], n = a.counts ? a.counts[w] : a.offsets[w + 1] - off;
         if (n == 0) {
             if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
             continue;
         }
+        if (a.sx) gather_window(a, w, off, n, gb, GB);
         const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
         // fresh accumulators for the window: every CTA is past the previous
         // window's last step before block 0 clears them
@@ -1688,11 +1726,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
     const int ntop = tree.top_lvl[tree.top_levels];
 
     for (int w = grp; w < a.n_windows; w += a.groups) {
-        const long long off = a.offsets[w], n = a.offsets[w + 1] - off;
+        const long long off = a.offsets[w], n = a.counts ? a.counts[w] : a.offsets[w + 1] - off;
         if (n == 0) {
             if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
             continue;
         }
+        if (a.sx) gather_window(a, w, off, n, gb, GB);
         const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
         if (kTraceBuild && a.trace && grp == 0 && w == 0 && gb == 0) trace_point(a, 0, -1);
         grid_sync(ctr, target, GB);

@@ -70,6 +70,48 @@ def _evd1():
     return z, json.loads(bytes(z["meta"]).decode())
 
 
+def _resident_bound(ctx, lo=-1.2, hi=-0.4):
+    """bound_terms of one interval over the context's resident window set."""
+    import ctypes
+    from paper_2209_13168_b200 import _lib
+    out = [np.zeros(1, dtype=np.uint64), np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.uint64)]
+    lo_a, hi_a = np.array([lo]), np.array([hi])
+    rc = ctx.lib.evd_bound_images(ctx.h, _lib.ptr(lo_a), _lib.ptr(hi_a), 1,
+                                  _lib.ptr(out[0], _lib._u64p), _lib.ptr(out[1], _lib._i64p),
+                                  _lib.ptr(out[2], _lib._u64p), ctypes.POINTER(ctypes.c_uint32)())
+    assert rc == 0
+    return [int(a[0]) for a in out]
+
+
+@pytest.mark.parametrize("chunk", [1024, 5000, 1 << 16])
+def test_stream_overlapped_upload(chunk):
+    """Host arrays: the raw stream is uploaded in chunks while the solve runs
+    (each window's group waits for its events); samples and the resident
+    window set equal the upload-then-solve path's, for pageable and pinned
+    inputs, with gaps and an offset start."""
+    import torch
+    from paper_2209_13168_b200 import _lib
+    s = _stream(n_desc=4)
+    keep = ((s.t < 1.2) | (s.t >= 2.9)) & (s.t >= 0.6)
+    g = EventStream(s.x[keep], s.y[keep], s.t[keep], s.polarity[keep], s.geometry)
+    params = evd.SolverParams()
+    ctx = _lib.Context(0)
+    ctx.set_option("stream_overlap", 0)
+    want = _key(evd.stream_divergence(g, params, ctx=ctx))
+    want_res = _resident_bound(ctx)
+    ctx.set_option("stream_overlap", 1)
+    ctx.set_option("stream_chunk", chunk)
+    got = evd.stream_divergence(g, params, ctx=ctx)
+    assert _key(got) == want
+    assert _resident_bound(ctx) == want_res
+    pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (g.x, g.y, g.t)]
+    gp = EventStream(*(p.numpy() for p in pinned), g.polarity, g.geometry)
+    assert _key(evd.stream_divergence(gp, params, ctx=ctx)) == want
+    assert _resident_bound(ctx) == want_res
+    with pytest.raises(_lib.EvdError):
+        ctx.set_option("stream_chunk", 10)
+
+
 def test_parse_event_bin_matches_reference():
     z, meta = _evd1()
     for name in meta["valid"]:
