@@ -397,9 +397,22 @@ def windows_line(ctx):
     from paper_2209_13168_b200 import solver as sol, synth
     batches = [synth.sequence_window(k) for k in range(2000)]
     sol.solve_windows(batches[:64], evd.SolverParams(), ctx=ctx)
+    # device time of the solve alone: upload first, then launch
+    ctx.set_option("stream_overlap", 0)
+    t0 = time.perf_counter()
     res, dev_s, groups = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
+    serial = time.perf_counter() - t0
+    # the public path: the upload overlapped with the solve (evd_solve_windows_list)
+    ctx.set_option("stream_overlap", 1)
+    t0 = time.perf_counter()
+    res2, _, _ = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
+    overlapped = time.perf_counter() - t0
+    same = [(r.nu, r.contrast, r.iterations) for r in res] == \
+        [(r.nu, r.contrast, r.iterations) for r in res2]
     return {"windows": len(batches), "events": int(sum(b.n for b in batches)),
             "device_s": dev_s, "windows_per_s": len(batches) / dev_s, "solver_groups": groups,
+            "e2e_s_upload_then_solve": serial, "e2e_s_overlapped": overlapped,
+            "overlapped_identical": same,
             "all_ok": all(r.status == 0 for r in res)}, batches
 
 

@@ -133,7 +133,10 @@ int evd_eval_frontier(evd_ctx *ctx, const double *lo, const double *hi, int32_t 
                       uint64_t *s_bar, int64_t *fully_inside, uint64_t *marks);
 
 /* Per-context options: "frontier_path" (EVD_FRONTIER_*), "frontier_image_budget"
- * (bytes of HBM images per global-path launch, default 8 GiB). */
+ * (bytes of HBM images per global-path launch, default 8 GiB), "stream_overlap"
+ * (1, default: evd_solve_stream / evd_solve_windows_list upload host events
+ * while the solve runs; 0: upload, then solve) and "stream_chunk" (events per
+ * upload chunk, 1024..262144, default 65536). */
 int evd_set_option(evd_ctx *ctx, const char *name, int64_t value);
 
 /* Diagnostics of the tiled frontier: out[0] tiles of the frame (0: not
@@ -202,12 +205,26 @@ int evd_solve_windows(evd_ctx *ctx, const int64_t *offsets, int32_t n_windows, i
                       const evd_solve_params *params, evd_window_result *results,
                       double *device_ms);
 
+/* evd_set_events_list + evd_solve_windows in one call, the upload overlapped
+ * with the solve: the solve is launched first, the host windows follow in
+ * chunks on a copy stream, and each window's solver group starts once its
+ * events have arrived (estimate_stream_divergence, solver.py:139-162, over a
+ * list of EventBatch).  Results and the resident window set afterwards are
+ * those of the two calls; device_ms includes the wait for the events. */
+int evd_solve_windows_list(evd_ctx *ctx, const double *const *x, const double *const *y,
+                           const double *const *t, const int64_t *counts, int32_t k,
+                           int32_t width, int32_t height, double tau, int32_t groups,
+                           const evd_solve_params *params, evd_window_result *results,
+                           double *device_ms);
+
 /* batch_stream + estimate_stream_divergence (events.py:330-359,
  * solver.py:139-162) for a whole time-sorted stream in one call: the raw
  * events go to the device once, the windows [k*tau, (k+1)*tau) are found by
- * binary search on the device, their events are gathered into the solve
- * layout (centred x, y; batch-local t = min(t - k*tau, tau)) and every window
- * is solved in one evd_solve_windows launch.  *n_windows = k1 - k0 + 1 (also
+ * binary search (on the host copy of t for host arrays, else on the device),
+ * their events are gathered into the solve layout (centred x, y; batch-local
+ * t = min(t - k*tau, tau)) and every window is solved in one evd_solve_windows
+ * launch.  Host arrays are uploaded while the solve runs ("stream_overlap"):
+ * each window's group gathers its events once they have arrived.  *n_windows = k1 - k0 + 1 (also
  * on EVD_ERR_ARG when `capacity` is too small), *k0 = floor(t[0] / tau);
  * results[w] describes window k0 + w (t_start = (k0 + w) * tau; status
  * EVD_ERR_NO_EVENTS for an empty window).  The stream becomes the context's

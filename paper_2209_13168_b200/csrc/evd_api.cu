@@ -1015,9 +1015,11 @@ constexpr long long kLargeWindow = 250000;    // 768-thread CTAs from this on
 // the device arrays k_solve / k_solve_spec gather from, and the host loop that
 // feeds them (issued once, right after the first launch).
 struct StreamFeed {
+    const double *sx, *sy, *st;       // device: the raw events as they arrive
     const long long *s_lo, *counts;   // device, per window
     const long long *h_counts;        // host copy of counts
     long long k0;
+    int t_local;                      // 1: t is window-local already (no shift)
     std::function<int()> upload;
 };
 
@@ -1129,9 +1131,10 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         a.spec_k = spec_k;
         if (feed) {
-            a.sx = ctx->sx.p;
-            a.sy = ctx->sy.p;
-            a.stt = ctx->st.p;
+            a.sx = feed->sx;
+            a.sy = feed->sy;
+            a.stt = feed->st;
+            a.t_local = feed->t_local;
             a.s_lo = feed->s_lo;
             a.counts = feed->counts;
             a.ready = ctx->feedw.p;
@@ -1368,45 +1371,38 @@ static long long host_lower_bound(const double *t, long long n, double v)
     return lo;
 }
 
-// evd_solve_stream from host arrays: the windows' bounds come from the host
-// copy of t, the solve is launched at once, and the raw stream follows in
-// chunks on ctx->copy (host memcpy into a ring of pinned slots, then H2D);
-// each window's group starts when its events have arrived.  The solve layout
-// pads every window to 16 events; once the solve is done the resident window
-// set is re-gathered unpadded (the evd_set_events contract).
-static int solve_stream_overlapped(evd_ctx *ctx, const double *x, const double *y,
-                                   const double *t, long long n, bool pinned, double tau,
-                                   int groups,
-                                   const evd_solve_params *params, evd_window_result *results,
-                                   int capacity, int32_t *n_windows, int64_t *k0_out,
-                                   double *device_ms)
+// Host event arrays in solve order: k pieces (one for a stream, one per window
+// for a window list), concatenated they are the raw events the solve gathers.
+struct HostPieces {
+    const double *const *x, *const *y, *const *t;
+    const long long *n;
+    int k;
+    bool pinned;  // one page-locked piece: DMA from it directly
+};
+
+// Solve windows whose raw events are still on the host, uploading them on
+// ctx->copy while the solve runs: chunks of the concatenated pieces go
+// through a ring of pinned slots (host memcpy, then H2D into dx / dy / dt),
+// each followed by the count of raw events delivered; window w's group waits
+// for its events (raw [lo[w], lo[w] + cnt[w])) and gathers them into the
+// solve layout, which pads every window to 16 events.  On return (success or
+// not) the copy stream is idle.
+static int solve_fed(evd_ctx *ctx, const HostPieces &src, long long total_raw, double *dx,
+                     double *dy, double *dt, const std::vector<long long> &lo,
+                     const std::vector<long long> &cnt, long long k0, bool t_local, int groups,
+                     const evd_solve_params *params, evd_window_result *results,
+                     double *device_ms)
 {
-    // events.py:341-342 on the host copy of t
-    const double f0 = std::floor(t[0] / tau), f1 = std::floor(t[n - 1] / tau);
-    if (!(f0 >= 0.0) || !(f1 >= f0) || f1 - f0 >= 2147483647.0)
-        return fail(ctx, EVD_ERR_ARG, "timestamps must be sorted, non-negative and finite");
-    const long long k0 = (long long)f0;
-    const int nw = (int)((long long)f1 - k0 + 1);
-    *n_windows = nw;
-    *k0_out = k0;
-    if (!results || capacity < nw)
-        return fail(ctx, EVD_ERR_ARG, "stream spans %d windows, results hold %d", nw, capacity);
-    std::vector<long long> lo(nw), cnt(nw), pad(nw + 1), o(nw + 1);
-    pad[0] = o[0] = 0;
-    for (int w = 0; w < nw; w++) {
-        const double start = (double)(k0 + w) * tau;
-        lo[w] = host_lower_bound(t, n, start);
-        cnt[w] = std::max(0LL, host_lower_bound(t, n, start + tau) - lo[w]);
-        o[w + 1] = o[w] + cnt[w];
-        pad[w + 1] = pad[w] + (cnt[w] + 15) / 16 * 16;
-    }
-    const long long total = o[nw];
+    const int nw = (int)cnt.size();
+    std::vector<long long> pad(nw + 1);
+    pad[0] = 0;
+    for (int w = 0; w < nw; w++) pad[w + 1] = pad[w] + (cnt[w] + 15) / 16 * 16;
     CU(ctx->xc.ensure(std::max(pad[nw], 1LL)));
     CU(ctx->yc.ensure(std::max(pad[nw], 1LL)));
     CU(ctx->t.ensure(std::max(pad[nw], 1LL)));
     CU(ctx->feedw.ensure(2));
     CU(ctx->feedb.ensure(3 * (size_t)nw + 1));
-    long long *d_lo = ctx->feedb.p, *d_cnt = d_lo + nw, *d_off = d_cnt + nw;
+    long long *d_lo = ctx->feedb.p, *d_cnt = d_lo + nw;
     if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
     if (!ctx->feed_start) {
         CU(cudaEventCreateWithFlags(&ctx->feed_start, cudaEventDisableTiming));
@@ -1423,66 +1419,109 @@ static int solve_stream_overlapped(evd_ctx *ctx, const double *x, const double *
     CU(cudaMemcpyAsync(d_lo, lo.data(), nw * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(d_cnt, cnt.data(), nw * sizeof(long long), cudaMemcpyHostToDevice,
                        ctx->stream));
-    CU(cudaMemcpyAsync(d_off, o.data(), (nw + 1) * sizeof(long long), cudaMemcpyHostToDevice,
-                       ctx->stream));
-    // the copies start after everything queued so far (earlier readers of sx / sy / st)
+    // the copies start after everything queued so far (earlier readers of dx / dy / dt)
     CU(cudaEventRecord(ctx->feed_start, ctx->stream));
     CU(cudaStreamWaitEvent(ctx->copy, ctx->feed_start, 0));
-    ctx->W = ctx->sW;
-    ctx->H = ctx->sH;
-    ctx->tau = tau;
-    ctx->gen++;
-    ctx->n = 0;  // the resident window set is rebuilt below
-    const long long S = std::min<long long>(ctx->feed_chunk, (long long)(2 * half / 8 / 32));
     const int slots = 8;
+    const long long S = std::min<long long>(ctx->feed_chunk, (long long)(2 * half / 8 / 32));
     const size_t slot_bytes = (size_t)S * 3 * sizeof(double) + 64;
-    StreamFeed feed{d_lo, d_cnt, cnt.data(), k0, nullptr};
+    StreamFeed feed{dx, dy, dt, d_lo, d_cnt, cnt.data(), k0, t_local ? 1 : 0, nullptr};
     feed.upload = [&]() -> int {
-        for (long long c0 = 0, c = 0; c0 < n; c0 += S, c++) {
+        int p = 0;             // piece and position in it of the next raw event
+        long long pp = 0;
+        for (long long c0 = 0, c = 0; c0 < total_raw; c0 += S, c++) {
             const int sl = (int)(c % slots);
             if (c >= slots) CU(cudaEventSynchronize(ctx->feed_ev[sl]));  // slot free again
-            const long long m = std::min(S, n - c0);
+            const long long m = std::min(S, total_raw - c0);
             double *px = reinterpret_cast<double *>(ctx->stage + sl * slot_bytes);
             double *py = px + S, *pt = py + S;
             unsigned long long *val = reinterpret_cast<unsigned long long *>(pt + S);
-            if (pinned) {  // page-locked already: DMA straight from the caller's arrays
-                px = const_cast<double *>(x + c0);
-                py = const_cast<double *>(y + c0);
-                pt = const_cast<double *>(t + c0);
+            if (src.pinned) {
+                px = const_cast<double *>(src.x[0] + c0);
+                py = const_cast<double *>(src.y[0] + c0);
+                pt = const_cast<double *>(src.t[0] + c0);
             } else {
-                memcpy(px, x + c0, m * sizeof(double));
-                memcpy(py, y + c0, m * sizeof(double));
-                memcpy(pt, t + c0, m * sizeof(double));
+                for (long long f = 0; f < m;) {
+                    while (pp == src.n[p]) {
+                        p++;
+                        pp = 0;
+                    }
+                    const long long take = std::min(m - f, src.n[p] - pp);
+                    memcpy(px + f, src.x[p] + pp, take * sizeof(double));
+                    memcpy(py + f, src.y[p] + pp, take * sizeof(double));
+                    memcpy(pt + f, src.t[p] + pp, take * sizeof(double));
+                    f += take;
+                    pp += take;
+                }
             }
             *val = (unsigned long long)(c0 + m);
-            CU(cudaMemcpyAsync(ctx->sx.p + c0, px, m * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx->copy));
-            CU(cudaMemcpyAsync(ctx->sy.p + c0, py, m * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx->copy));
-            CU(cudaMemcpyAsync(ctx->st.p + c0, pt, m * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx->copy));
+            CU(cudaMemcpyAsync(dx + c0, px, m * sizeof(double), cudaMemcpyHostToDevice, ctx->copy));
+            CU(cudaMemcpyAsync(dy + c0, py, m * sizeof(double), cudaMemcpyHostToDevice, ctx->copy));
+            CU(cudaMemcpyAsync(dt + c0, pt, m * sizeof(double), cudaMemcpyHostToDevice, ctx->copy));
             CU(cudaMemcpyAsync(ctx->feedw.p, val, sizeof *val, cudaMemcpyHostToDevice, ctx->copy));
             CU(cudaEventRecord(ctx->feed_ev[sl], ctx->copy));
         }
         return EVD_OK;
     };
+    long long live = 0;
+    for (int w = 0; w < nw; w++) live += cnt[w];
     int rc = EVD_OK;
-    if (total == 0) {  // every window empty: nothing to solve, the stream still goes up
-        if ((rc = feed.upload())) return rc;
+    if (live == 0) {  // every window empty: nothing to solve, the events still go up
+        rc = feed.upload();
         for (int w = 0; w < nw; w++) {
             results[w] = evd_window_result{};
             results[w].status = EVD_ERR_NO_EVENTS;
         }
         if (device_ms) *device_ms = 0.0;
-    } else if ((rc = solve_offsets(ctx, pad.data(), nw, groups, params, results, device_ms,
-                                   &feed))) {
-        CU(cudaStreamSynchronize(ctx->copy));
-        return rc;
+    } else {
+        rc = solve_offsets(ctx, pad.data(), nw, groups, params, results, device_ms, &feed);
     }
-    // the copy stream is done (every window waited for its chunk, or the empty
-    // case): resident window set = the windows concatenated, unpadded
     CU(cudaStreamSynchronize(ctx->copy));
+    return rc;
+}
+
+// evd_solve_stream from host arrays: the windows' bounds come from the host
+// copy of t (k_window_bounds' search), the raw stream follows the launch
+// (solve_fed), and the resident window set is re-gathered unpadded afterwards
+// (the evd_set_events contract).
+static int solve_stream_overlapped(evd_ctx *ctx, const double *x, const double *y,
+                                   const double *t, long long n, bool pinned, double tau,
+                                   int groups, const evd_solve_params *params,
+                                   evd_window_result *results, int capacity, int32_t *n_windows,
+                                   int64_t *k0_out, double *device_ms)
+{
+    // events.py:341-342 on the host copy of t
+    const double f0 = std::floor(t[0] / tau), f1 = std::floor(t[n - 1] / tau);
+    if (!(f0 >= 0.0) || !(f1 >= f0) || f1 - f0 >= 2147483647.0)
+        return fail(ctx, EVD_ERR_ARG, "timestamps must be sorted, non-negative and finite");
+    const long long k0 = (long long)f0;
+    const int nw = (int)((long long)f1 - k0 + 1);
+    *n_windows = nw;
+    *k0_out = k0;
+    if (!results || capacity < nw)
+        return fail(ctx, EVD_ERR_ARG, "stream spans %d windows, results hold %d", nw, capacity);
+    std::vector<long long> lo(nw), cnt(nw), o(nw + 1);
+    o[0] = 0;
+    for (int w = 0; w < nw; w++) {
+        const double start = (double)(k0 + w) * tau;
+        lo[w] = host_lower_bound(t, n, start);
+        cnt[w] = std::max(0LL, host_lower_bound(t, n, start + tau) - lo[w]);
+        o[w + 1] = o[w] + cnt[w];
+    }
+    ctx->W = ctx->sW;
+    ctx->H = ctx->sH;
+    ctx->tau = tau;
+    ctx->gen++;
+    ctx->n = 0;  // the resident window set is rebuilt below
+    const HostPieces src{&x, &y, &t, &n, 1, pinned};
+    int rc = solve_fed(ctx, src, n, ctx->sx.p, ctx->sy.p, ctx->st.p, lo, cnt, k0, false, groups,
+                       params, results, device_ms);
+    if (rc) return rc;
+    const long long total = o[nw];
     if (total > 0) {
+        long long *d_lo = ctx->feedb.p, *d_off = d_lo + 2 * nw;
+        CU(cudaMemcpyAsync(d_off, o.data(), (nw + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                           ctx->stream));
         launch_gather_windows(ctx->sx.p, ctx->sy.p, ctx->st.p, d_lo, d_off, nw, k0, total, tau,
                               ctx->sW / 2.0, ctx->sH / 2.0, ctx->xc.p, ctx->yc.p, ctx->t.p,
                               ctx->stream);
@@ -1490,6 +1529,63 @@ static int solve_stream_overlapped(evd_ctx *ctx, const double *x, const double *
         CU(cudaStreamSynchronize(ctx->stream));
     }
     ctx->n = total;
+    ctx->gen++;
+    return EVD_OK;
+}
+
+int evd_solve_windows_list(evd_ctx *ctx, const double *const *x, const double *const *y,
+                           const double *const *t, const int64_t *counts, int32_t k,
+                           int32_t width, int32_t height, double tau, int32_t groups,
+                           const evd_solve_params *params, evd_window_result *results,
+                           double *device_ms)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (k < 0 || width < 1 || height < 1 || !params || (k > 0 && (!x || !y || !t || !counts || !results)))
+        return fail(ctx, EVD_ERR_ARG, "bad evd_solve_windows_list arguments");
+    if (int rc = check_frame(ctx, width, height)) return rc;
+    if (!(tau > 0.0)) return fail(ctx, EVD_ERR_ARG, "batch duration tau must be positive");
+    long long n = 0;
+    std::vector<long long> lo(k), cnt(k);
+    for (int w = 0; w < k; w++) {
+        if (counts[w] < 0 || (counts[w] > 0 && (!x[w] || !y[w] || !t[w])))
+            return fail(ctx, EVD_ERR_ARG, "bad window %d", w);
+        lo[w] = n;
+        cnt[w] = counts[w];
+        n += counts[w];
+    }
+    if (device_ms) *device_ms = 0.0;
+    CU(cudaSetDevice(ctx->device));
+    if (!ctx->stream_overlap) {  // upload, then solve
+        if (int rc = evd_set_events_list(ctx, x, y, t, counts, k, width, height, tau)) return rc;
+        if (k == 0) return EVD_OK;
+        std::vector<long long> o(k + 1);
+        o[0] = 0;
+        for (int w = 0; w < k; w++) o[w + 1] = o[w] + cnt[w];
+        return solve_offsets(ctx, o.data(), k, groups, params, results, device_ms);
+    }
+    CU(ctx->wx.ensure(std::max(n, 1LL)));
+    CU(ctx->wy.ensure(std::max(n, 1LL)));
+    CU(ctx->wt.ensure(std::max(n, 1LL)));
+    ctx->W = width;
+    ctx->H = height;
+    ctx->tau = tau;
+    ctx->gen++;
+    ctx->n = 0;  // the resident window set is rebuilt below
+    if (k == 0) return EVD_OK;
+    const HostPieces src{x, y, t, reinterpret_cast<const long long *>(counts), k, false};
+    int rc = solve_fed(ctx, src, n, ctx->wx.p, ctx->wy.p, ctx->wt.p, lo, cnt, 0, true, groups,
+                       params, results, device_ms);
+    if (rc) return rc;
+    // resident window set = the windows concatenated (as evd_set_events_list leaves it)
+    if (n > 0) {
+        launch_center(ctx->wx.p, ctx->wy.p, n, width / 2.0, height / 2.0, ctx->xc.p, ctx->yc.p,
+                      ctx->stream);
+        LAUNCHED(1);
+        CU(cudaMemcpyAsync(ctx->t.p, ctx->wt.p, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->n = n;
     ctx->gen++;
     return EVD_OK;
 }

@@ -101,6 +101,7 @@ struct SolveArgs {
     const unsigned long long *ready;
     double *gx, *gy, *gt;         // xc / yc / t, writable
     long long k0;
+    int t_local;                  // t already window-local: gathered unchanged
     unsigned int *stall;          // set when an upload never arrived (the window is garbage)
 };
 constexpr long long kUploadTimeoutNs = 20000000000ll;  // 20 s

@@ -831,10 +831,11 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     __syncthreads();
 }
 
-// Overlapped stream upload: the group of window w waits (thread 0 of each
-// CTA) until the copy stream has delivered the window's raw events, then
-// gathers them into the solve layout with k_gather_windows' arithmetic
-// (centred x, y; t - start capped at tau, events.py:348).  The raw stream is
+// Overlapped upload: the group of window w waits (thread 0 of each CTA)
+// until the copy stream has delivered the window's raw events, then gathers
+// them into the solve layout with k_gather_windows' arithmetic (centred x, y;
+// stream windows: t - start capped at tau, events.py:348; window lists: t as
+// given, evd_set_events_list).  The raw stream is
 // read through L2 (__ldcg: written by the copy engine during this kernel);
 // the gathered region is read by the group only after the grid barrier that
 // follows, and no other window shares its cache lines (padded offsets).
@@ -863,8 +864,8 @@ __device__ __noinline__ void gather_window(const SolveArgs &a, int w, long long 
         const long long i = lo + j;
         a.gx[off + j] = dsub(__ldcg(a.sx + i), a.cx);
         a.gy[off + j] = dsub(__ldcg(a.sy + i), a.cy);
-        const double d = dsub(__ldcg(a.stt + i), start);
-        a.gt[off + j] = d < a.tau ? d : a.tau;
+        const double tr = __ldcg(a.stt + i), d = dsub(tr, start);
+        a.gt[off + j] = a.t_local ? tr : (d < a.tau ? d : a.tau);
     }
 }
 

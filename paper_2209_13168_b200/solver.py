@@ -157,25 +157,20 @@ def solve_windows(batches: list[EventBatch], params: SolverParams, groups: int =
         raise ValueError("solve_windows needs windows of one geometry and tau")
     velocity_domain(tau, params.epsilon)
     sizes = np.array([b.n for b in batches], dtype=np.int64)
-    offsets = np.zeros(len(batches) + 1, dtype=np.int64)
-    np.cumsum(sizes, out=offsets[1:])
     ctx = ctx or _lib.context()
-    # every window's arrays straight to the device (evd_set_events_list: pinned
-    # staging, no host concatenation)
+    # every window's arrays straight to the device while the solve runs
+    # (evd_solve_windows_list: pinned staging, no host concatenation, each
+    # window's solver group starts once its events have arrived)
     cols = [[_lib.f64(getattr(b, k)) for b in batches] for k in ("x", "y", "t")]
     ptrs = [(_lib._d * len(batches))(*[_lib.ptr(a) for a in col]) for col in cols]
-    rc = ctx.lib.evd_set_events_list(ctx.h, ptrs[0], ptrs[1], ptrs[2],
-                                     _lib.ptr(sizes, _lib._i64p), len(batches), g0.width,
-                                     g0.height, tau)
-    if rc:
-        _raise(ctx, rc)
-    ctx._resident = None
     p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
                          float(params.min_interval_width), int(params.max_iterations))
     res = (_lib.WindowResult * len(batches))()
     ms = (ctypes.c_double * 1)()
-    rc = ctx.lib.evd_solve_windows(ctx.h, _lib.ptr(offsets, _lib._i64p), len(batches),
-                                   int(groups), p, res, ms)
+    ctx._resident = None
+    rc = ctx.lib.evd_solve_windows_list(ctx.h, ptrs[0], ptrs[1], ptrs[2],
+                                        _lib.ptr(sizes, _lib._i64p), len(batches), g0.width,
+                                        g0.height, tau, int(groups), p, res, ms)
     if rc:
         _raise(ctx, rc)
     return list(res), ms[0] / 1e3, (res[0].groups if len(batches) else 0)

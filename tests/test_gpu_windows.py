@@ -103,3 +103,42 @@ def test_dist_batched_over_nccl_world1():
     ref = pdist.solve_batched(b, evd.SolverParams(), k=16)
     assert (got.nu, got.contrast, got.bound_gap, got.rounds, got.nodes) == (
         ref.nu, ref.contrast, ref.bound_gap, ref.rounds, ref.nodes)
+
+
+@pytest.mark.parametrize("chunk", [1024, 7000, 1 << 16])
+def test_windows_list_overlapped_upload(chunk):
+    """evd_solve_windows_list: the solve starts before the host windows are
+    uploaded (chunks spanning window boundaries, an empty window between);
+    results and the resident window set afterwards equal upload-then-solve."""
+    import ctypes
+    g = SensorGeometry(240, 180)
+    batches = [synth.sequence_window(k) for k in range(20, 29)]
+    batches.insert(4, EventBatch(np.empty(0), np.empty(0), np.empty(0), batches[0].tau, g))
+    ctx = _lib.Context(0)
+
+    def resident():
+        out = [np.zeros(1, dtype=np.uint64), np.zeros(1, dtype=np.int64),
+               np.zeros(1, dtype=np.uint64)]
+        lo, hi = np.array([-1.5]), np.array([-0.3])
+        rc = ctx.lib.evd_bound_images(ctx.h, _lib.ptr(lo), _lib.ptr(hi), 1,
+                                      _lib.ptr(out[0], _lib._u64p), _lib.ptr(out[1], _lib._i64p),
+                                      _lib.ptr(out[2], _lib._u64p),
+                                      ctypes.POINTER(ctypes.c_uint32)())
+        assert rc == 0
+        return [int(a[0]) for a in out]
+
+    ctx.set_option("stream_overlap", 0)
+    want, _, _ = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
+    want_res = resident()
+    ctx.set_option("stream_overlap", 1)
+    ctx.set_option("stream_chunk", chunk)
+    got, secs, _ = sol.solve_windows(batches, evd.SolverParams(), ctx=ctx)
+    assert secs > 0
+    key = lambda rs: [(r.status, r.nu, r.contrast, r.bound_gap, r.iterations) for r in rs]
+    assert key(got) == key(want)
+    assert got[4].status == _lib.EVD_ERR_NO_EVENTS
+    assert resident() == want_res
+    # every window empty: no solve, statuses only
+    empties = [batches[4]] * 3
+    res, _, _ = sol.solve_windows(empties, evd.SolverParams(), ctx=ctx)
+    assert all(r.status == _lib.EVD_ERR_NO_EVENTS for r in res)
