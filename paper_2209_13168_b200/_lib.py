@@ -150,6 +150,8 @@ def load():
                     f"g.build()'` (make -C paper_2209_13168_b200/csrc)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("EVD_LIB") and not hasattr(lib, name):
+                    continue  # an older build under A/B (tools/ab_libs.sh)
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

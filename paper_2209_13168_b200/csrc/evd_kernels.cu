@@ -1264,7 +1264,9 @@ struct SolveSmem {
     static constexpr size_t region_a = queue > kStepBytes ? queue : kStepBytes;
 };
 
-template <bool FILTER, int NT>
+// FEED: the windows arrive during the launch (SolveArgs' overlapped upload);
+// a separate instantiation so the resident-window kernels keep their code
+template <bool FILTER, int NT, bool FEED = false>
 __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 {
     constexpr size_t kRegionA = SolveSmem<NT>::region_a;
@@ -1315,12 +1317,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
     if (tracer && gb == 0) trace_point(a, 0, -1);
 
     for (int w = grp; w < a.n_windows; w += a.groups) {
-        const long long off = a.offsets[w], n = a.counts ? a.counts[w] : a.offsets[w + 1] - off;
+        const long long off = a.offsets[w], n = FEED ? a.counts[w] : a.offsets[w + 1] - off;
         if (n == 0) {
             if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
             continue;
         }
-        if (a.sx) gather_window(a, w, off, n, gb, GB);
+        if (FEED) gather_window(a, w, off, n, gb, GB);
         const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
         // fresh accumulators for the window: every CTA is past the previous
         // window's last step before block 0 clears them
@@ -1603,7 +1605,10 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 // ~3.5x less often.  The frontier is replicated in every CTA's shared memory.
 constexpr int kSpecFr = 1024;     // frontier entries per CTA (shared memory)
 constexpr int kSpecCache = 64;    // results of evaluated, not yet popped nodes
-constexpr double kSpecWidth = 1.0;  // only intervals this narrow are speculated (all but the root)
+#ifndef EVD_SPEC_WIDTH
+#define EVD_SPEC_WIDTH 1.0
+#endif
+constexpr double kSpecWidth = EVD_SPEC_WIDTH;  // only intervals this narrow are speculated
 
 struct SpecSlot {
     double lo, hi, c, den_lo, den_c, den_hi;
@@ -1686,7 +1691,7 @@ __device__ __forceinline__ void spec_set_slot(const SolveArgs &a, SpecSlot &s,
     s.counter = e.counter & ~kSpecFlag;
 }
 
-template <int NT>
+template <int NT, bool FEED = false>
 __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
 {
     constexpr size_t kRegionA = SolveSmem<NT>::region_a;
@@ -1727,12 +1732,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
     const int ntop = tree.top_lvl[tree.top_levels];
 
     for (int w = grp; w < a.n_windows; w += a.groups) {
-        const long long off = a.offsets[w], n = a.counts ? a.counts[w] : a.offsets[w + 1] - off;
+        const long long off = a.offsets[w], n = FEED ? a.counts[w] : a.offsets[w + 1] - off;
         if (n == 0) {
             if (gb == 0 && threadIdx.x == 0) a.res[w].status = kStatusEmpty;
             continue;
         }
-        if (a.sx) gather_window(a, w, off, n, gb, GB);
+        if (FEED) gather_window(a, w, off, n, gb, GB);
         const double *xc = a.xc + off, *yc = a.yc + off, *tw = a.t + off;
         if (kTraceBuild && a.trace && grp == 0 && w == 0 && gb == 0) trace_point(a, 0, -1);
         grid_sync(ctr, target, GB);
@@ -2117,6 +2122,10 @@ static void set_attrs()
                          (int)solve_smem<768>());
     cudaFuncSetAttribute(k_solve<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)solve_smem<512>());
+    cudaFuncSetAttribute(k_solve<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)solve_smem<512>());
+    cudaFuncSetAttribute(k_solve_spec<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)spec_smem<512>());
     cudaFuncSetAttribute(k_event_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kQueueBytes);
     cudaFuncSetAttribute(k_solve_spec<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2252,12 +2261,14 @@ cudaError_t launch_solve_spec(const SolveArgs &a, int blocks, int threads, cudaS
     set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
-    const void *fn = threads == 384 ? (const void *)k_solve_spec<384>
+    // the overlapped-upload variant (a.sx set) is built at 512 threads only
+    if (a.sx || (threads != 384 && threads != 768)) threads = 512;
+    const void *fn = a.sx           ? (const void *)k_solve_spec<512, true>
+                   : threads == 384 ? (const void *)k_solve_spec<384>
                    : threads == 768 ? (const void *)k_solve_spec<768>
                                     : (const void *)k_solve_spec<512>;
     const size_t smem = threads == 384 ? spec_smem<384>()
                       : threads == 768 ? spec_smem<768>() : spec_smem<512>();
-    if (threads != 384 && threads != 768) threads = 512;
     return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(threads), params, smem, s);
 }
 
@@ -2266,9 +2277,11 @@ cudaError_t launch_solve(const SolveArgs &a, int blocks, int threads, cudaStream
     set_attrs();
     SolveArgs args = a;
     void *params[] = {&args};
-    // the filtered path (opt-in) is built at 512 threads only
-    if (a.filter || (threads != 384 && threads != 768)) threads = 512;
-    const void *fn = a.filter         ? (const void *)k_solve<true, 512>
+    // the filtered path (opt-in) and the overlapped-upload variant (a.sx set)
+    // are built at 512 threads only
+    if (a.filter || a.sx || (threads != 384 && threads != 768)) threads = 512;
+    const void *fn = a.sx             ? (const void *)k_solve<false, 512, true>
+                   : a.filter         ? (const void *)k_solve<true, 512>
                    : threads == 384   ? (const void *)k_solve<false, 384>
                    : threads == 768   ? (const void *)k_solve<false, 768>
                                       : (const void *)k_solve<false, 512>;
