@@ -58,6 +58,7 @@ def main():
         "seconds_per_call": t, "median_s": float(np.median(times)),
         "events_x_bound_evals_per_s": units / t,
         "marks": marks, "marks_per_event_interval": marks / units,
+        "checksum": [int(s.astype(np.uint64).sum(dtype=np.uint64)), int(fi.sum())],
         "atomics_per_s": marks / t, "atomic_peak": apk,
         "atomic_frac": (marks / t / 1e9 / apk) if apk else None,
         "launches_per_call": launches, "path": path, "info": ctx.frontier_info(),
