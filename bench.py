@@ -640,6 +640,10 @@ def run_gpu(args, rank, world, local):
         if nc:
             limiter = {
                 "kind": "latency / issue (sequential BnB rounds; per-warp dependent chains)",
+                "atomic_roof_binding": False,
+                "atomic_evidence": "profiles/no_red_ab_r02.txt: segment REDs compiled out "
+                                   "(-DEVD_NO_RED) change the event pass by <= 1% at the cfg-2 "
+                                   "root (144.0 -> 143.2 us) and narrow nodes (10.2 -> 10.0 us)",
                 "issue_active_pct": ncu_val(nc, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 "warps_active_pct": ncu_val(nc, "sm__warps_active.avg.pct_of_peak_sustained_active"),
                 "fp64_pipe_pct": ncu_val(nc, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),

@@ -81,7 +81,11 @@ struct AtomicSink {
     unsigned int *img;
     __device__ __forceinline__ void operator()(long long p, int, int) const
     {
+#ifdef EVD_NO_RED  // timing experiment only (profiles/no_red_ab_r02.txt): WRONG images
+        if (p == -12345) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(img + p));
+#else
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(img + p));
+#endif
     }
 };
 
