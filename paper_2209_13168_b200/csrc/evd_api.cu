@@ -1054,6 +1054,10 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     int spec_k = GB < 32 ? 1 : (max_n < kSmallWindow ? 3 : (max_n < kSpecMaxEvents ? 4 : 2));
     if (const char *e = getenv("EVD_SPEC_K")) spec_k = std::max(1, std::min(kSpecK, atoi(e)));
     if (ctx->trace_on && !getenv("EVD_TRACE_SPEC")) spec_k = 1;  // EVD_TRACE_SPEC=1: rounds
+    // k_solve_spec certifies the root bound instead of rasterising it
+    // (kModeRootCert) unless the root is narrower than min_interval_width
+    // (then its exact bound is the result's bound_gap, solver.py:106-108)
+    int root_cert = (hi0 - lo0 < params->min_interval_width || getenv("EVD_NO_ROOT_CERT")) ? 0 : 1;
     // CTA size: small windows on the whole grid are latency-bound (384 fatter
     // threads), large ones sampler-throughput-bound (768); grouped solves and
     // the traced build stay at 512 (measured: cfg 1 1.10 -> 1.04 ms at 384,
@@ -1130,6 +1134,7 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         a.filter = (max_n >= kFilterMinEvents) ? 1 : 0;
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         a.spec_k = spec_k;
+        a.root_cert = root_cert;
         if (feed) {
             a.sx = feed->sx;
             a.sy = feed->sy;
@@ -1176,11 +1181,16 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
             CU(cudaStreamSynchronize(ctx->stream));
             if (stall) return fail(ctx, EVD_ERR_CUDA, "stream upload did not arrive in time");
         }
-        bool again = false, overflow = false;
+        bool again = false, overflow = false, uncertified = false;
         for (int w : todo) {
             out[w] = got[w];
             if (got[w].status == kStatusCapacity) again = true;
             if (got[w].status == kStatusSpecOverflow) overflow = true;
+            if (got[w].status == kStatusRootCert) uncertified = true;
+        }
+        if (uncertified) {  // a root bound near c_hat + gamma: rerun with it rasterised
+            root_cert = 0;
+            continue;
         }
         if (overflow) {  // the shared-memory frontier filled up: rerun without speculation
             spec_k = 1;

@@ -63,6 +63,49 @@ __device__ __forceinline__ int fully_inside(double ax, double ay, double bx, dou
             0.0 <= bx && bx < W && 0.0 <= by && by < H) ? 1 : 0;
 }
 
+// Root-bound certificate (k_solve_spec, kModeRootCert).  A lower bound on the
+// number of in-frame pixels the reference marks for the closed segment
+// a -> b (contrast.py:94-182): clip it to the frame (approximately), shrink
+// its extent by a margin far above any rounding of the reference's own clip
+// and samples, and count the integers x = k strictly inside the shrunk
+// x-extent (nx; likewise ny).  Each such line is crossed by the segment, so
+// the reference's midpoint samples visit nx + 1 distinct columns, all inside
+// the frame (ceil(lo) >= 1, floor(hi) <= W - 1), and mark a pixel of each
+// (a sample on y = H also marks its row H - 1 square): >= max(nx, ny) + 1
+// pixels when that maximum is positive.  Summed over events this bounds
+// sum(counts) from below, and sum(counts^2) >= sum(counts)^2 / M.
+__device__ __forceinline__ unsigned int root_cells_lb(double ax, double ay, double bx, double by,
+                                                      int W, int H)
+{
+    const double dx = bx - ax, dy = by - ay;
+    double t0 = 0.0, t1 = 1.0;
+    if (dx == 0.0) {
+        if (ax < 0.0 || ax > W) return 0;
+    } else {
+        double ta = -ax / dx, tb = (W - ax) / dx;
+        if (ta > tb) { const double u = ta; ta = tb; tb = u; }
+        t0 = fmax(t0, ta);
+        t1 = fmin(t1, tb);
+    }
+    if (dy == 0.0) {
+        if (ay < 0.0 || ay > H) return 0;
+    } else {
+        double ta = -ay / dy, tb = (H - ay) / dy;
+        if (ta > tb) { const double u = ta; ta = tb; tb = u; }
+        t0 = fmax(t0, ta);
+        t1 = fmin(t1, tb);
+    }
+    if (!(t0 < t1)) return 0;
+    const double x0 = ax + t0 * dx, x1 = ax + t1 * dx, y0 = ay + t0 * dy, y1 = ay + t1 * dy;
+    constexpr double m = 1e-6;
+    const double xl = fmax(fmin(x0, x1), 0.0) + m, xh = fmin(fmax(x0, x1), (double)W) - m;
+    const double yl = fmax(fmin(y0, y1), 0.0) + m, yh = fmin(fmax(y0, y1), (double)H) - m;
+    const double nx = xh > xl ? floor(xh) - ceil(xl) + 1.0 : 0.0;
+    const double ny = yh > yl ? floor(yh) - ceil(yl) + 1.0 : 0.0;
+    const double k = fmax(nx, ny);
+    return k > 0.0 ? (unsigned int)k + 1u : 0u;
+}
+
 // ---------------------------------------------------------------- filtered path
 // Approximate warp with r = RN(1/denom) (correctly rounded, computed once per
 // velocity): s~ = RN(num * r) is within 3 ulp-relative of the exact

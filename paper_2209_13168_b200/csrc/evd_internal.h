@@ -32,7 +32,9 @@ struct alignas(32) FrontierEntry {
     double lo, hi;
 };
 
-enum SolveMode : int { kModeRoot = 0, kModeNode = 1 };
+// kModeRootCert: the root round evaluates the root as a node (both children)
+// and certifies its bound instead of rasterising it (k_solve_spec)
+enum SolveMode : int { kModeRoot = 0, kModeNode = 1, kModeRootCert = 2 };
 enum SolveStatus : int { kStatusOk = 0, kStatusIterLimit = 1, kStatusCapacity = 2 };
 
 // Device-resident BnB state (one per context); host reads it back at the end.
@@ -59,7 +61,9 @@ struct SolveState {
 };
 
 // Result of one window of evd_solve_windows / evd_solve.
-enum WindowStatus : int { kStatusEmpty = 3, kStatusSpecOverflow = 4 };
+// kStatusRootCert: the root bound could not be certified (the host reruns
+// with the root rasterised)
+enum WindowStatus : int { kStatusEmpty = 3, kStatusSpecOverflow = 4, kStatusRootCert = 5 };
 struct WindowResult {
     double nu, contrast, bound_gap;
     long long iterations, bound_evals, point_evals, max_fr;
@@ -90,6 +94,7 @@ struct SolveArgs {
     long long *btrace;            // [kBTraceIters][group_blocks][kBTraceSlots] (or null)
     int filter;                   // use the filtered (approximate-then-exact) event path
     int spec_k;                   // k_solve_spec: evaluations per round (1..kSpecK)
+    int root_cert;                // k_solve_spec: certify the root bound (kModeRootCert)
     // Overlapped stream upload (evd_solve_stream from host arrays; sx null:
     // the windows are already gathered).  The raw stream arrives in chunks on
     // a copy stream while the solve runs; *ready = raw events on the device.

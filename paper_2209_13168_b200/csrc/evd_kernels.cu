@@ -890,6 +890,9 @@ struct EventJob {
     long long gsz;
     int gb;
     int guided;  // shrink claims as the counter runs out (wide nodes)
+    // kModeRootCert: [0] += root_cells_lb, [1] += fully_inside of the root
+    // segment (the root bound's certificate, k_solve_spec)
+    unsigned long long *acc_root;
 };
 
 template <int C = kChunk>
@@ -915,6 +918,7 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
     // batches of up to 32 events, fewer when the window cannot give every warp
     // one full batch: a small window is latency-bound, and more, shorter
     // batches keep all warps busy (cfg 1: 20k events on 2368 warps)
+    unsigned long long rc0 = 0, rc1 = 0;  // kModeRootCert
     long long fb = n / (EVD_BATCH_DIV * warps);
     const int first = (int)(fb < 4 ? 4 : (fb > 32 ? 32 : fb));
     long long base = (j.gb * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * first;
@@ -936,6 +940,10 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
                 v[1] += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
                 cA = segment_or_queue<C>(wl.x, wl.y, wh.x, wh.y, W, H, wq, 2 * lane, sa, dummy);
             } else {
+                if (j.mode == kModeRootCert) {
+                    rc0 += root_cells_lb(wl.x, wl.y, wh.x, wh.y, W, H);
+                    rc1 += fully_inside(wl.x, wl.y, wh.x, wh.y, W, H);
+                }
                 v[1] += fully_inside(wl.x, wl.y, wc.x, wc.y, W, H);
                 cA = segment_or_queue<C>(wl.x, wl.y, wc.x, wc.y, W, H, wq, 2 * lane, sa, dummy);
                 v[2] += fully_inside(wc.x, wc.y, wh.x, wh.y, W, H);
@@ -954,6 +962,14 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
         long long nb = 0;
         if (lane == 0) nb = warps * first + (long long)atomicAdd(acc + 7, (unsigned long long)size);
         base = __shfl_sync(0xffffffffu, nb, 0);
+    }
+    if (j.mode == kModeRootCert) {
+        rc0 = warp_sum(rc0);
+        rc1 = warp_sum(rc1);
+        if (lane == 0) {
+            if (rc0) atomicAdd(j.acc_root, rc0);
+            if (rc1) atomicAdd(j.acc_root + 1, rc1);
+        }
     }
 }
 
@@ -1636,6 +1652,7 @@ struct SpecState {
     int ncache, cache_head;
     int cur;  // cache index of the node being processed (-1: slot results below)
     int rounds;
+    int root_ok;  // kModeRootCert: the root bound is certified to exceed c_hat + gamma
 };
 
 // Frontier entries already chosen for a speculative slot carry this bit in
@@ -1753,7 +1770,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
         if (threadIdx.x == 0) {
             Z.slot[0] = SpecSlot{a.lo0, a.hi0, a.c0, a.den_lo0, a.den_c0, a.den_hi0, -1};
             Z.nslot = 1;
-            Z.mode = kModeRoot;
+            Z.mode = a.root_cert ? kModeRootCert : kModeRoot;
+            Z.root_ok = 0;
             Z.done = 0;
             Z.status = kStatusOk;
             Z.parity = 0;
@@ -1781,7 +1799,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 unsigned long long v[4] = {0, 0, 0, 0}, vex[1] = {0};
                 EventJob J{xc, yc, tw, n, sl.lo, sl.c, sl.hi, sl.den_lo, sl.den_c, sl.den_hi,
                            a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
-                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth};
+                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1]};
                 event_pass_exact<chunk_for(NT)>(J, wq, v, vex);
 #pragma unroll
                 for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);
@@ -1924,6 +1942,18 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                         Z.mu[0] = cbA;  // the root bound
                         continue;
                     }
+                    if (s == 0 && mode == kModeRootCert) {
+                        // solver.py:92-108 pushes the root with c_bar = S/M - mu_lower^2
+                        // and pops it at once; only gap > gamma matters, and
+                        // S >= (sum of root_cells_lb)^2 / M, mu_lower = fi / M
+                        // (Cauchy-Schwarz over the M pixels), with a relative
+                        // margin far above the reference's rounding of c_bar
+                        const double Md = (double)M;
+                        const double q = (double)__ldcg(&sacc[1][0]) / Md;
+                        const double f = (double)__ldcg(&sacc[1][1]) / Md;
+                        const double L = (q * q - f * f) * (1.0 - 1e-9);
+                        Z.root_ok = (L - Cs > a.gamma + 1e-9 * fabs(Cs)) ? 1 : 0;
+                    }
                     SpecRes &r = Z.cache[Z.cache_head];
                     r.counter = Z.slot[s].counter;
                     r.C = Cs;
@@ -1945,7 +1975,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 // from the same shared-memory reads); lane 0 writes the
                 // frontier entries and, at the end, the state back to Z.
                 SpecSlot node = Z.slot[0];
-                bool root = mode == kModeRoot;
+                bool root = mode == kModeRoot, rootc = mode == kModeRootCert;
                 int stop = 0, next_uncached = 0;
                 double c_hat = Z.c_hat, nu_hat = Z.nu_hat, bound_gap = Z.bound_gap;
                 int fr_n = (int)Z.fr_n, cur = Z.cur, status = Z.status;
@@ -1969,6 +1999,25 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                         point_evals++;
                         bound_evals++;
                         push(Z.mu[0], node.lo, node.hi);
+                    } else if (rootc) {
+                        // solver.py:92-108 with the root bound certified: the
+                        // root is pushed and popped (gap > gamma, width >=
+                        // min_width, checked on the host), then evaluated from
+                        // its cached result like any node
+                        c_hat = Z.cache[cur].C;  // contrast_at(domain.center)
+                        nu_hat = node.c;
+                        point_evals++;
+                        bound_evals++;
+                        if (fr_n + 1 > max_fr) max_fr = fr_n + 1;
+                        next_counter++;
+                        if (!Z.root_ok) {
+                            status = kStatusRootCert;
+                            stop = 1;
+                            break;
+                        }
+                        iterations++;
+                        rootc = false;
+                        continue;
                     } else {  // solver.py:109-119
                         const SpecRes &r = Z.cache[cur];
                         point_evals++;

@@ -320,3 +320,40 @@ def test_bound_validity_properties_full_size(cfg):
         assert np.array_equal(ims[2], pim[0])
         assert [int(ims[j].sum(dtype=np.uint64)) for j in range(3)] == [int(m) for m in marks]
         assert fi[2] == ins[0]
+
+
+@pytest.mark.parametrize("cert", ["on", "off"])
+def test_root_certificate(bnb_golden, monkeypatch, cert, rng):
+    """The speculative solve certifies the root bound (S >= (sum of per-event
+    cell lower bounds)^2 / M) instead of rasterising it; a window whose
+    certificate fails (few events: the bound is not provably above c_hat +
+    gamma) is rerun with the root rasterised.  Results equal the reference's
+    either way, including iteration limits at the root and a root narrower
+    than min_interval_width (whose exact bound is the reported bound_gap)."""
+    if cert == "off":
+        monkeypatch.setenv("EVD_NO_ROOT_CERT", "1")
+    monkeypatch.setenv("EVD_SPEC_K", "4")
+    meta, windows = bnb_golden
+    for w, batch in windows:
+        assert _same(evd.maximise_contrast_bnb(batch, evd.SolverParams()), w["result"])
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        gold = json.load(fh)
+    for cfg in ("1", "2"):
+        r, st = sol.solve_window(synth.config_window(int(cfg)), evd.SolverParams())
+        assert _same(r, gold["configs"][cfg]["result"])
+    # certificate failures: 1-6 events, and a dense tiny frame
+    for n in (1, 2, 3, 6):
+        b = random_batch(rng, 16, 12, n)
+        o = orc.maximise_contrast_bnb(b)
+        r = evd.maximise_contrast_bnb(b, evd.SolverParams())
+        assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (o.nu, o.contrast, o.bound_gap,
+                                                                 o.iterations)
+    b = synth.config_window(1)
+    with pytest.raises(evd.IterationLimitError) as err:
+        evd.maximise_contrast_bnb(b, evd.SolverParams(max_iterations=1))
+    o = orc.maximise_contrast_bnb(b, max_iterations=1)
+    assert (err.value.nu, err.value.contrast, err.value.iterations) == (o.nu, o.contrast, 1)
+    small = windows[0][1]
+    r = evd.maximise_contrast_bnb(small, evd.SolverParams(min_interval_width=3.0))
+    o = orc.maximise_contrast_bnb(small, min_interval_width=3.0)
+    assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (o.nu, o.contrast, o.bound_gap, 1)
