@@ -458,9 +458,11 @@ def windows_dist_leg(batches, world, reps=3):
 
 def cfg5_leg(world, rank):
     """Config 5 (1280x720, 5,327,641 events): the single-GPU device-resident
-    exact solve (maximise_contrast_bnb) and dist.solve_batched_dist on the N
+    exact solve (maximise_contrast_bnb), dist.solve_batched_dist on the N
     ranks (events broadcast once over NCCL, each round's evaluations split
-    over the ranks, results all-gathered; certified within gamma)."""
+    over the ranks, results all-gathered; certified within gamma) and
+    dist.solve_spec_dist (the same split, replaying the reference's pops
+    exactly)."""
     import torch
     import paper_2209_13168_b200 as evd
     from paper_2209_13168_b200 import dist as pdist, synth
@@ -484,6 +486,20 @@ def cfg5_leg(world, rank):
                       "nodes": rb.nodes, "bound_evals": rb.bound_evals, "k": 64}
     if rank == 0:
         out["batched_within_gamma"] = rb.contrast >= out["exact"]["contrast"] - params.gamma
+    # the exact speculative split solve: the reference's pops, each round's
+    # node evaluations (4 per rank) split over the ranks
+    pdist.solve_spec_dist(batch, params, slots_per_rank=4)  # warm-up
+    barrier_all(world)
+    t0 = time.perf_counter()
+    rs = pdist.solve_spec_dist(batch, params, slots_per_rank=4)
+    barrier_all(world)
+    out["spec_dist_e2e_s"] = max_over_ranks(world, time.perf_counter() - t0)
+    out["spec_dist"] = {"nu": rs.nu, "contrast": rs.contrast, "iterations": rs.iterations,
+                        "rounds": rs.rounds, "node_evals": rs.node_evals,
+                        "slots": 4 * world}
+    if rank == 0:
+        out["spec_dist_identical"] = (rs.nu, rs.contrast, rs.iterations) == (
+            r.nu, r.contrast, r.iterations)
     return out
 
 

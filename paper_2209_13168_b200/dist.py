@@ -243,5 +243,123 @@ def solve_batched(batch, params, k: int = 64, contrasts: Callable | None = None,
     return BatchedResult(nu_hat, c_hat, gap_out, rounds, nodes, evals)
 
 
+# ------------------------------------------------------------------ exact speculative split BnB
+@dataclass(frozen=True)
+class SpecResult:
+    nu: float
+    contrast: float
+    bound_gap: float
+    iterations: int      # the reference's pops (identical to maximise_contrast_bnb)
+    rounds: int          # evaluation rounds (one split evaluation + all-gather each)
+    node_evals: int      # nodes evaluated (centre + both children), speculation included
+    bound_evals: int     # bound evaluations made (root + children of evaluated nodes)
+
+
+def solve_spec(batch, params, slots: int = 8, contrasts: Callable | None = None,
+               bounds: Callable | None = None, group=None, split: bool = False) -> SpecResult:
+    """The reference's best-first BnB (solver.py:79-123) replayed exactly,
+    with node evaluations batched speculatively -- the host form of
+    k_solve_spec's rounds, made to spread over ranks.
+
+    A node's results (centre contrast, both child bounds) are a pure function
+    of its interval, so they can be computed before the reference pops it.
+    Each round evaluates ``slots`` nodes: the node the replay must pop next
+    (the first one not yet evaluated) and the best other open entries that
+    could still be popped (bound above c_hat + gamma, width >= the minimum).
+    The replay then pops in the reference's order -- heap key (-c_bar,
+    push counter), incumbent update with >=, pruning with >=, the iteration
+    cap after the node -- for as long as the popped nodes are evaluated.
+    ``split``: each round's centres and child intervals are divided over the
+    ranks of ``group`` (events replicated; ``_split_eval``) and all-gathered,
+    so every rank holds the same cache and replays the same pops.  Results,
+    including the pop count, are the reference's on any number of ranks.
+    """
+    from .solver import IterationLimitError
+
+    if contrasts is None or bounds is None:
+        contrasts, bounds = gpu_evaluators(batch)
+    ev_c = (lambda nus: _split_eval(contrasts, (nus,), group)) if split else contrasts
+    ev_b = (lambda lo, hi: _split_eval(bounds, (lo, hi), group)) if split else bounds
+    dom = velocity_domain(batch.tau, params.epsilon)
+    cache: dict[tuple[float, float], tuple[float, float, float]] = {}
+    rounds = node_evals = 0
+    bound_evals = 1
+
+    def evaluate(nodes, extra=()):
+        nonlocal rounds, node_evals, bound_evals
+        cen = [0.5 * (lo + hi) for lo, hi in nodes]  # VelocityInterval.center
+        lo_b = [v for (lo, hi), c in zip(nodes, cen) for v in (lo, c)] + [a for a, _ in extra]
+        hi_b = [v for (lo, hi), c in zip(nodes, cen) for v in (c, hi)] + [b for _, b in extra]
+        cc = np.asarray(ev_c(np.array(cen, dtype=np.float64)))
+        cb = np.asarray(ev_b(np.array(lo_b, dtype=np.float64), np.array(hi_b, dtype=np.float64)))
+        for j, node in enumerate(nodes):
+            cache[node] = (float(cc[j]), float(cb[2 * j]), float(cb[2 * j + 1]))
+        rounds += 1
+        node_evals += len(nodes)
+        bound_evals += 2 * len(nodes)
+        return [float(v) for v in cb[2 * len(nodes):]]
+
+    root = (dom.lo, dom.hi)
+    # round 0: the root's bound (solver.py:96-98) and the root as a node; the
+    # centre contrast is the initial incumbent (solver.py:93-94)
+    root_bound = evaluate([root], extra=[root])[0]
+    nu_hat, c_hat = dom.center, cache[root][0]
+    ctr = itertools.count()
+    heap = [(-root_bound, next(ctr), dom.lo, dom.hi)]
+    iterations = 0
+    bound_gap = 0.0
+    while heap:
+        neg, _, lo, hi = heap[0]
+        gap = -neg - c_hat
+        if gap <= params.gamma or hi - lo < params.min_interval_width:  # solver.py:105-108
+            iterations += 1
+            bound_gap = max(gap, 0.0)
+            break
+        if (lo, hi) not in cache:
+            # next round: this node, then the best open entries the replay may pop
+            todo = [(lo, hi)]
+            for e in heapq.nsmallest(len(heap), heap):
+                if len(todo) >= slots:
+                    break
+                elo, ehi = e[2], e[3]
+                if (elo, ehi) in cache or (elo, ehi) == (lo, hi):
+                    continue
+                if -e[0] - c_hat <= params.gamma or ehi - elo < params.min_interval_width:
+                    continue  # popping it ends the search: never evaluated
+                todo.append((elo, ehi))
+            evaluate(todo)
+        heapq.heappop(heap)
+        iterations += 1
+        cen = 0.5 * (lo + hi)
+        c_c, cb_lo, cb_hi = cache[(lo, hi)]
+        if c_c >= c_hat:  # solver.py:111-113
+            nu_hat, c_hat = cen, c_c
+        for clo, chi, b in ((lo, cen, cb_lo), (cen, hi, cb_hi)):
+            if b >= c_hat:  # solver.py:116
+                heapq.heappush(heap, (-b, next(ctr), clo, chi))
+        if iterations >= params.max_iterations:  # solver.py:118-119
+            raise IterationLimitError(nu_hat, c_hat, iterations)
+    return SpecResult(nu_hat, c_hat, bound_gap, iterations, rounds, node_evals, bound_evals)
+
+
+def solve_spec_dist(batch, params, slots_per_rank: int = 4, group=None,
+                    src: int = 0) -> SpecResult:
+    """``solve_spec`` over the ranks of ``group`` on GPUs: the window's events
+    broadcast once from ``src`` (NCCL) and loaded from device memory, each
+    round's ``slots_per_rank * world`` node evaluations split over the ranks.
+    Every rank returns the identical, reference-exact result."""
+    import torch.distributed as dist
+    from types import SimpleNamespace
+
+    from .contrast import load_window_device
+    x, y, t, tau, geometry = broadcast_window(batch, group, src)
+    ctx = load_window_device(x, y, t, tau, geometry)
+    view = SimpleNamespace(n=int(t.numel()), tau=tau, geometry=geometry)
+    contrasts, bounds = gpu_evaluators(view, ctx=ctx)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    return solve_spec(view, params, slots=slots_per_rank * world, contrasts=contrasts,
+                      bounds=bounds, group=group, split=world > 1)
+
+
 def divergence_of(result, tau: float) -> float:
     return divergence_from_velocity(result.nu, tau)

@@ -74,8 +74,17 @@ def _worker(rank, world, port, queue):
         x, y, t, tau, geom = pdist.broadcast_window(b if rank == 0 else None)
         same = (np.array_equal(x.numpy(), b.x) and np.array_equal(y.numpy(), b.y) and
                 np.array_equal(t.numpy(), b.t) and tau == b.tau and geom == b.geometry)
+        # the exact speculative solve, each round's evaluations split over the ranks
+        sp = pdist.solve_spec(b, params, slots=6, contrasts=c, bounds=bd, split=True)
+        try:
+            pdist.solve_spec(b, SolverParams(max_iterations=4), slots=4, contrasts=c, bounds=bd,
+                             split=True)
+            sp_cap = None
+        except IterationLimitError as e:
+            sp_cap = (e.nu, e.contrast, e.iterations)
         queue.put((rank, [(s.t, s.contrast, s.iterations) for s in samples],
-                   (res.nu, res.contrast, res.rounds, res.nodes), same, capped))
+                   (res.nu, res.contrast, res.rounds, res.nodes), same, capped,
+                   (sp.nu, sp.contrast, sp.bound_gap, sp.iterations, sp.rounds), sp_cap))
     finally:
         dist.destroy_process_group()
 
@@ -102,7 +111,13 @@ def test_world2_gloo_windows_and_split_frontier():
         p.join(timeout=60)
         assert p.exitcode == 0
     outs.sort(key=lambda o: o[0])
-    (_, s0, r0, b0, c0), (_, s1, r1, b1, c1) = outs
+    (_, s0, r0, b0, c0, p0, q0), (_, s1, r1, b1, c1, p1, q1) = outs
+    # the split speculative solve is the reference's, pop for pop, on both ranks
+    bw = _windows()[1]
+    ref = orc.maximise_contrast_bnb(bw)
+    assert p0 == p1 and p0[:4] == (ref.nu, ref.contrast, ref.bound_gap, ref.iterations)
+    refc = orc.maximise_contrast_bnb(bw, max_iterations=4)
+    assert q0 == q1 == (refc.nu, refc.contrast, 4)
     # both ranks hold the full, identical sample list and the identical BnB state
     assert s0 == s1 and r0 == r1
     # both ranks stop at the cap with the same incumbent
@@ -143,3 +158,48 @@ def test_batched_iteration_cap_carries_incumbent():
             pdist.solve_batched(b, SolverParams(max_iterations=cap), k=4, contrasts=c, bounds=bd)
         assert ei.value.iterations == cap
         assert ei.value.contrast <= full.contrast
+
+
+@pytest.mark.parametrize("slots", [1, 3, 16])
+def test_spec_solve_is_the_reference(bnb_golden, slots):
+    """solve_spec replays the reference's pops exactly (nu, contrast,
+    bound_gap and pop count bit-identical to the pinned oracle) for any number
+    of speculative slots per round; more slots, fewer rounds."""
+    meta, windows = bnb_golden
+    rounds = []
+    for w, b in windows[:6]:
+        c, bd = _oracle_evaluators(b)
+        r = pdist.solve_spec(b, SolverParams(), slots=slots, contrasts=c, bounds=bd)
+        assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (
+            f64(w["result"]["nu"]), f64(w["result"]["contrast"]), f64(w["result"]["bound_gap"]),
+            w["result"]["iterations"])
+        assert r.node_evals >= r.iterations - 1 and r.rounds <= r.iterations
+        rounds.append((r.rounds, r.node_evals))
+    if slots == 1:  # one node per round: the reference's own sequence of evaluations
+        assert all(rd == ne for rd, ne in rounds)
+
+
+def test_spec_solve_edges():
+    """Iteration cap after the node that reaches it (incumbent carried), a
+    root narrower than min_interval_width (its exact bound is the gap), and a
+    window of one event."""
+    b = _windows()[1]
+    c, bd = _oracle_evaluators(b)
+    for cap in (1, 2, 7):
+        ref = orc.maximise_contrast_bnb(b, max_iterations=cap)
+        if ref.status != "iteration_limit":
+            continue
+        with pytest.raises(IterationLimitError) as ei:
+            pdist.solve_spec(b, SolverParams(max_iterations=cap), slots=5, contrasts=c, bounds=bd)
+        assert (ei.value.nu, ei.value.contrast, ei.value.iterations) == (ref.nu, ref.contrast, cap)
+    ref = orc.maximise_contrast_bnb(b, min_interval_width=3.0)
+    r = pdist.solve_spec(b, SolverParams(min_interval_width=3.0), slots=4, contrasts=c, bounds=bd)
+    assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (ref.nu, ref.contrast, ref.bound_gap,
+                                                             ref.iterations)
+    from paper_2209_13168_b200.events import EventBatch, SensorGeometry
+    one = EventBatch(np.array([3.5]), np.array([2.25]), np.array([0.1]), 0.5, SensorGeometry(8, 6))
+    c1, b1 = _oracle_evaluators(one)
+    ref = orc.maximise_contrast_bnb(one)
+    r = pdist.solve_spec(one, SolverParams(), slots=4, contrasts=c1, bounds=b1)
+    assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (ref.nu, ref.contrast, ref.bound_gap,
+                                                             ref.iterations)

@@ -105,6 +105,32 @@ def test_dist_batched_over_nccl_world1():
         ref.nu, ref.contrast, ref.bound_gap, ref.rounds, ref.nodes)
 
 
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_spec_dist_solve_is_the_reference(cfg):
+    """dist.solve_spec_dist (NCCL broadcast, libevd evaluators from device
+    memory, speculative rounds) gives the reference's BnbResult, pop count
+    included, at configs 1 and 2."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2209_13168_b200 import dist as pdist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        b = synth.config_window(cfg)
+        got = pdist.solve_spec_dist(b, evd.SolverParams(), slots_per_rank=6)
+    finally:
+        dist.destroy_process_group()
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        ref = json.load(fh)["configs"][str(cfg)]["result"]
+    assert (got.nu, got.contrast, got.bound_gap, got.iterations) == (
+        f64(ref["nu"]), f64(ref["contrast"]), f64(ref["bound_gap"]), ref["iterations"])
+
+
 @pytest.mark.parametrize("chunk", [1024, 7000, 1 << 16])
 def test_windows_list_overlapped_upload(chunk):
     """evd_solve_windows_list: the solve starts before the host windows are
