@@ -180,6 +180,17 @@ typedef struct {
                              when speculative rounds evaluated several nodes at once */
 } evd_solve_result;
 
+/* The per-node work of maximise_contrast_bnb (solver.py:109-117) for k nodes
+ * [lo[i], hi[i]] of the resident window: contrast_at(center) and
+ * bound_terms(child).c_bar of both halves (VelocityInterval.split,
+ * geometry.py:40-46), bit-identical to the reference's values; the nodes run
+ * through the solve kernel's speculative rounds (several per event pass),
+ * without a search.  Used by the host-driven exact BnB that splits a round's
+ * nodes over GPUs (dist.solve_spec).  EVD_ERR_CHEIRALITY for an inadmissible
+ * endpoint. */
+int evd_eval_nodes(evd_ctx *ctx, const double *lo, const double *hi, int64_t k,
+                   double *contrast, double *cbar_lo, double *cbar_hi);
+
 /* Whole solve on the device for the resident window (one cooperative
  * persistent launch).  Returns EVD_ERR_ITER_LIMIT with the incumbent in *res
  * when max_iterations is reached. */

@@ -252,6 +252,27 @@ def bound_terms(batch: EventBatch, interval: VelocityInterval) -> ContrastBound:
     return assemble_bound(int(s_bar[0]), int(fi[0]), batch.geometry.n_pixels)
 
 
+def node_terms(batch: EventBatch, lo, hi, ctx=None, loaded=False):
+    """The per-node work of maximise_contrast_bnb (solver.py:109-117) for the
+    nodes [lo[i], hi[i]]: contrast_at(center) and both children's c_bar
+    (evd_eval_nodes: the solve kernel's rounds, several nodes per event pass).
+
+    Returns (contrast float64[k], cbar_lo float64[k], cbar_hi float64[k]).
+    """
+    lo = _lib.f64(np.atleast_1d(lo))
+    hi = _lib.f64(np.atleast_1d(hi))
+    if lo.shape != hi.shape:
+        raise ValueError("lo and hi differ in length")
+    ctx = ctx if loaded else load_window(batch, ctx)
+    k = lo.size
+    con, ca, cb = (np.empty(k, dtype=np.float64) for _ in range(3))
+    rc = ctx.lib.evd_eval_nodes(ctx.h, _lib.ptr(lo), _lib.ptr(hi), k, _lib.ptr(con),
+                                _lib.ptr(ca), _lib.ptr(cb))
+    if rc:
+        _raise(ctx, rc)
+    return con, ca, cb
+
+
 def frontier_terms(batch: EventBatch, lo, hi, ctx=None, loaded=False):
     """Batched frontier: exact bound integers for k intervals in one pass.
 

@@ -77,6 +77,7 @@ struct evd_ctx {
     DevBuf<unsigned int> simg;         // solve images, per group (always left zeroed)
     DevBuf<unsigned long long> acc;    // 8 accumulators
     DevBuf<double> dscratch;           // misc device doubles
+    DevBuf<double> evbuf;              // evd_eval_nodes: lo | hi | results
     DevBuf<double> wx, wy, wt, wxo, wyo;
     DevBuf<double> segs, fargs;
     DevBuf<unsigned int> fimg;          // batched-frontier images (kept zeroed)
@@ -454,7 +455,7 @@ void evd_destroy(evd_ctx *ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf<double> *b : {&ctx->xc, &ctx->yc, &ctx->t, &ctx->dscratch, &ctx->wx, &ctx->wy,
+    for (DevBuf<double> *b : {&ctx->xc, &ctx->yc, &ctx->t, &ctx->dscratch, &ctx->evbuf, &ctx->wx, &ctx->wy,
                               &ctx->wt, &ctx->wxo, &ctx->wyo, &ctx->segs, &ctx->pow2})
         b->release();
     ctx->fargs.release();
@@ -1023,9 +1024,16 @@ struct StreamFeed {
     std::function<int()> upload;
 };
 
+// evd_eval_nodes: node intervals (device) and their results (device, 3 each)
+struct EvalList {
+    const double *lo, *hi;
+    long long n;
+    double *out;
+};
+
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
                        const evd_solve_params *params, std::vector<WindowResult> &out,
-                       float *ms_out, StreamFeed *feed = nullptr)
+                       float *ms_out, StreamFeed *feed = nullptr, const EvalList *ev = nullptr)
 {
     int rc;
     if (!(params->gamma > 0.0)) return fail(ctx, EVD_ERR_ARG, "gamma must be positive");
@@ -1058,6 +1066,7 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
     // (kModeRootCert) unless the root is narrower than min_interval_width
     // (then its exact bound is the result's bound_gap, solver.py:106-108)
     int root_cert = (hi0 - lo0 < params->min_interval_width || getenv("EVD_NO_ROOT_CERT")) ? 0 : 1;
+    if (ev) root_cert = 0;
     // CTA size: small windows on the whole grid are latency-bound (384 fatter
     // threads), large ones sampler-throughput-bound (768); grouped solves and
     // the traced build stay at 512 (measured: cfg 1 1.10 -> 1.04 ms at 384,
@@ -1135,6 +1144,12 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         if (const char *f = getenv("EVD_SOLVE_FILTER")) a.filter = (f[0] == '1');  // tests / tuning
         a.spec_k = spec_k;
         a.root_cert = root_cert;
+        if (ev) {
+            a.ev_lo = ev->lo;
+            a.ev_hi = ev->hi;
+            a.ev_n = ev->n;
+            a.ev_out = ev->out;
+        }
         if (feed) {
             a.sx = feed->sx;
             a.sy = feed->sy;
@@ -1150,7 +1165,7 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
             a.k0 = feed->k0;
         }
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU((spec_k > 1 || getenv("EVD_SPEC_FORCE"))
+        CU((spec_k > 1 || ev || getenv("EVD_SPEC_FORCE"))
                ? launch_solve_spec(a, groups * GB, threads, ctx->stream)
                : launch_solve(a, groups * GB, threads, ctx->stream));
         LAUNCHED(1);
@@ -1207,6 +1222,48 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
 }  // namespace
 
 extern "C" {
+
+int evd_eval_nodes(evd_ctx *ctx, const double *lo, const double *hi, int64_t k,
+                   double *contrast, double *cbar_lo, double *cbar_hi)
+{
+    if (!ctx) return fail(nullptr, EVD_ERR_ARG, "ctx is NULL");
+    if (k < 0 || (k > 0 && (!lo || !hi || !contrast || !cbar_lo || !cbar_hi)))
+        return fail(ctx, EVD_ERR_ARG, "bad node list");
+    int rc = need_events(ctx);
+    if (rc) return rc;
+    if (k == 0) return EVD_OK;
+    if (ctx->n == 0) return fail(ctx, EVD_ERR_NO_EVENTS, "no events in batch");
+    for (int64_t i = 0; i < k; i++) {
+        if (!(lo[i] <= hi[i]))
+            return fail(ctx, EVD_ERR_ARG, "empty interval [%.17g, %.17g]", lo[i], hi[i]);
+        double d;
+        if ((rc = check_den(ctx, lo[i], ctx->tau, &d))) return rc;
+        if ((rc = check_den(ctx, hi[i], ctx->tau, &d))) return rc;
+    }
+    CU(cudaSetDevice(ctx->device));
+    CU(ctx->evbuf.ensure((size_t)(5 * k)));
+    std::vector<double> h(2 * k);
+    std::copy(lo, lo + k, h.begin());
+    std::copy(hi, hi + k, h.begin() + k);
+    CU(cudaMemcpyAsync(ctx->evbuf.p, h.data(), 2 * k * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    const EvalList ev{ctx->evbuf.p, ctx->evbuf.p + k, k, ctx->evbuf.p + 2 * k};
+    const evd_solve_params params{1.0, 1e-6, 0.0, 1};  // unused by an evaluation-only launch
+    const long long off[2] = {0, ctx->n};
+    std::vector<WindowResult> out;
+    float ms = 0.f;
+    if ((rc = run_windows(ctx, off, 1, 1, &params, out, &ms, nullptr, &ev))) return rc;
+    std::vector<double> r(3 * k);
+    CU(cudaMemcpyAsync(r.data(), ev.out, 3 * k * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < k; i++) {
+        contrast[i] = r[3 * i];
+        cbar_lo[i] = r[3 * i + 1];
+        cbar_hi[i] = r[3 * i + 2];
+    }
+    return EVD_OK;
+}
 
 int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res)
 {

@@ -95,6 +95,12 @@ struct SolveArgs {
     int filter;                   // use the filtered (approximate-then-exact) event path
     int spec_k;                   // k_solve_spec: evaluations per round (1..kSpecK)
     int root_cert;                // k_solve_spec: certify the root bound (kModeRootCert)
+    // evaluation-only launch (evd_eval_nodes; k_solve_spec, one window): the
+    // nodes [ev_lo[i], ev_hi[i]] in rounds of spec_k slots, no BnB step;
+    // ev_out[3 i .. 3 i + 2] = contrast at the centre, c_bar of both children
+    const double *ev_lo, *ev_hi;
+    long long ev_n;
+    double *ev_out;
     // Overlapped stream upload (evd_solve_stream from host arrays; sx null:
     // the windows are already gathered).  The raw stream arrives in chunks on
     // a copy stream while the solve runs; *ready = raw events on the device.

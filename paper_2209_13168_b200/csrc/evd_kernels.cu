@@ -1716,7 +1716,9 @@ struct SpecState {
     int cur;  // cache index of the node being processed (-1: slot results below)
     int rounds;
     int root_ok;  // kModeRootCert: the root bound is certified to exceed c_hat + gamma
+    long long ev_next;  // evaluation-only launch: nodes handed to slots so far
 };
+
 
 // Frontier entries already chosen for a speculative slot carry this bit in
 // their counter (set by the round's slot selection, masked wherever the
@@ -1773,6 +1775,20 @@ __device__ __forceinline__ void spec_set_slot(const SolveArgs &a, SpecSlot &s,
     s.den_c = dadd(1.0, dmul(c, a.tau));
     s.den_hi = dadd(1.0, dmul(e.hi, a.tau));
     s.counter = e.counter & ~kSpecFlag;
+}
+
+// evaluation-only launch: the next round's slots from the node list
+__device__ __forceinline__ void spec_eval_slots(const SolveArgs &a, SpecState &Z, int K)
+{
+    int ns = 0;
+    while (ns < K && Z.ev_next < a.ev_n) {
+        const long long i = Z.ev_next++;
+        spec_set_slot(a, Z.slot[ns], FrontierEntry{0.0, i, a.ev_lo[i], a.ev_hi[i]});
+        ns++;
+    }
+    Z.nslot = ns;
+    Z.mode = kModeNode;
+    if (ns == 0) Z.done = 1;
 }
 
 template <int NT, bool FEED = false>
@@ -1839,6 +1855,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
             Z.mode = a.root_cert ? kModeRootCert : kModeRoot;
             Z.root_ok = 0;
             Z.done = 0;
+            Z.ev_next = 0;
+            if (a.ev_n > 0) spec_eval_slots(a, Z, K);
             Z.status = kStatusOk;
             Z.parity = 0;
             Z.nu_hat = Z.c_hat = Z.bound_gap = 0.0;
@@ -2030,12 +2048,23 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                     if (Z.ncache < kSpecCache) Z.ncache++;
                 }
                 if (Z.status == kStatusSpecOverflow) Z.done = 1;
+                if (a.ev_n > 0) {  // evaluation only: results out, next slots in
+                    if (gb == 0)
+                        for (int s = 0; s < ns; s++) {
+                            const long long i = Z.ev_next - ns + s;
+                            a.ev_out[3 * i] = s_res[s][0];
+                            a.ev_out[3 * i + 1] = s_res[s][1];
+                            a.ev_out[3 * i + 2] = s_res[s][2];
+                        }
+                    Z.parity = par ^ 1;
+                    spec_eval_slots(a, Z, K);
+                }
             }
             __syncthreads();
 #ifdef EVD_STEP_PROBE
             if (tr && gb == 0) trace_point(a, it, kTrMarks);
 #endif
-            if (threadIdx.x < 32 && !Z.done) {
+            if (threadIdx.x < 32 && !Z.done && a.ev_n == 0) {
                 // warp 0: the pop loop.  The BnB state lives in registers,
                 // identical in every lane (each lane computes the same values
                 // from the same shared-memory reads); lane 0 writes the

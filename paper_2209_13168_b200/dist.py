@@ -106,6 +106,19 @@ def gpu_evaluators(batch, ctx=None):
     return contrasts, bounds
 
 
+def gpu_node_evaluator(batch, ctx=None):
+    """nodes (lo[], hi[]) -> (centre contrasts, child c_bar lo, child c_bar
+    hi) on this process's GPU, several nodes per event pass (evd_eval_nodes)."""
+    from .contrast import load_window, node_terms
+
+    ctx = ctx if ctx is not None else load_window(batch)
+
+    def nodes(lo, hi):
+        return node_terms(batch, lo, hi, ctx=ctx, loaded=True)
+
+    return nodes
+
+
 def _coll_device(group):
     """Tensor device for collectives: the rank's GPU under NCCL, else the CPU."""
     import torch
@@ -115,10 +128,11 @@ def _coll_device(group):
     return torch.device("cpu")
 
 
-def _split_eval(fn, args, group):
+def _split_eval(fn, args, group, per_item: int = 1):
     """Evaluate fn over the items of ``args`` split round-robin over the ranks
     and all-gather the results (identical arrays on every rank): one padded
-    float64 tensor per rank, all-gathered over the group's backend."""
+    float64 tensor per rank, all-gathered over the group's backend.  fn
+    returns ``per_item`` values per item, item-major."""
     import torch
     import torch.distributed as dist
 
@@ -129,17 +143,17 @@ def _split_eval(fn, args, group):
     mine = np.arange(rank, n, world)
     vals = np.asarray(fn(*[np.asarray(a)[mine] for a in args]), dtype=np.float64) if len(mine) else \
         np.empty(0)
-    width = -(-n // world)  # ceil: rank r holds items r, r + world, ...
+    width = -(-n // world) * per_item  # ceil: rank r holds items r, r + world, ...
     dev = _coll_device(group)
     local = torch.zeros(width, dtype=torch.float64, device=dev)
     local[: len(vals)] = torch.from_numpy(vals).to(dev)
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local, group=group)
-    out = np.empty(n, dtype=np.float64)
+    out = np.empty((n, per_item), dtype=np.float64)
     for r, part in enumerate(parts):
         idx = np.arange(r, n, world)
-        out[idx] = part[: len(idx)].cpu().numpy()
-    return out
+        out[idx] = part[: len(idx) * per_item].cpu().numpy().reshape(-1, per_item)
+    return out.ravel() if per_item > 1 else out[:, 0]
 
 
 def broadcast_window(batch, group=None, src: int = 0):
@@ -256,7 +270,8 @@ class SpecResult:
 
 
 def solve_spec(batch, params, slots: int = 8, contrasts: Callable | None = None,
-               bounds: Callable | None = None, group=None, split: bool = False) -> SpecResult:
+               bounds: Callable | None = None, group=None, split: bool = False,
+               nodes: Callable | None = None) -> SpecResult:
     """The reference's best-first BnB (solver.py:79-123) replayed exactly,
     with node evaluations batched speculatively -- the host form of
     k_solve_spec's rounds, made to spread over ranks.
@@ -269,40 +284,54 @@ def solve_spec(batch, params, slots: int = 8, contrasts: Callable | None = None,
     The replay then pops in the reference's order -- heap key (-c_bar,
     push counter), incumbent update with >=, pruning with >=, the iteration
     cap after the node -- for as long as the popped nodes are evaluated.
-    ``split``: each round's centres and child intervals are divided over the
-    ranks of ``group`` (events replicated; ``_split_eval``) and all-gathered,
-    so every rank holds the same cache and replays the same pops.  Results,
+    ``split``: each round's nodes are divided over the ranks of ``group``
+    (events replicated; ``_split_eval``) and their results all-gathered, so
+    every rank holds the same cache and replays the same pops.  Results,
     including the pop count, are the reference's on any number of ranks.
+
+    Evaluators: ``nodes(lo[], hi[]) -> (contrast[], cbar_lo[], cbar_hi[])``
+    (one call per round, e.g. ``gpu_node_evaluator``), else ``contrasts`` and
+    ``bounds`` (two calls per round); ``bounds`` also gives the root's bound.
     """
     from .solver import IterationLimitError
 
-    if contrasts is None or bounds is None:
+    if bounds is None or (nodes is None and contrasts is None):
         contrasts, bounds = gpu_evaluators(batch)
-    ev_c = (lambda nus: _split_eval(contrasts, (nus,), group)) if split else contrasts
-    ev_b = (lambda lo, hi: _split_eval(bounds, (lo, hi), group)) if split else bounds
+    if nodes is None:
+        def nodes(lo, hi):
+            cen = 0.5 * (lo + hi)  # VelocityInterval.center, elementwise
+            cb = np.asarray(bounds(np.stack([lo, cen], 1).ravel(), np.stack([cen, hi], 1).ravel()))
+            return np.asarray(contrasts(cen)), cb[0::2], cb[1::2]
+
+    def node_rows(lo, hi):  # item-major (contrast, cbar_lo, cbar_hi) per node
+        return np.stack([np.asarray(v, np.float64) for v in nodes(lo, hi)], 1).ravel()
+
+    def ev_nodes(lo, hi):
+        flat = _split_eval(node_rows, (lo, hi), group, per_item=3) if split else node_rows(lo, hi)
+        return np.asarray(flat, np.float64).reshape(-1, 3)
+
     dom = velocity_domain(batch.tau, params.epsilon)
     cache: dict[tuple[float, float], tuple[float, float, float]] = {}
     rounds = node_evals = 0
     bound_evals = 1
 
-    def evaluate(nodes, extra=()):
+    def evaluate(todo):
         nonlocal rounds, node_evals, bound_evals
-        cen = [0.5 * (lo + hi) for lo, hi in nodes]  # VelocityInterval.center
-        lo_b = [v for (lo, hi), c in zip(nodes, cen) for v in (lo, c)] + [a for a, _ in extra]
-        hi_b = [v for (lo, hi), c in zip(nodes, cen) for v in (c, hi)] + [b for _, b in extra]
-        cc = np.asarray(ev_c(np.array(cen, dtype=np.float64)))
-        cb = np.asarray(ev_b(np.array(lo_b, dtype=np.float64), np.array(hi_b, dtype=np.float64)))
-        for j, node in enumerate(nodes):
-            cache[node] = (float(cc[j]), float(cb[2 * j]), float(cb[2 * j + 1]))
+        r = ev_nodes(np.array([a for a, _ in todo], dtype=np.float64),
+                     np.array([b for _, b in todo], dtype=np.float64))
+        for j, node in enumerate(todo):
+            cache[node] = (float(r[j, 0]), float(r[j, 1]), float(r[j, 2]))
         rounds += 1
-        node_evals += len(nodes)
-        bound_evals += 2 * len(nodes)
-        return [float(v) for v in cb[2 * len(nodes):]]
+        node_evals += len(todo)
+        bound_evals += 2 * len(todo)
 
     root = (dom.lo, dom.hi)
-    # round 0: the root's bound (solver.py:96-98) and the root as a node; the
-    # centre contrast is the initial incumbent (solver.py:93-94)
-    root_bound = evaluate([root], extra=[root])[0]
+    # round 0: the root's bound (solver.py:96-98, split like any evaluation)
+    # and the root as a node, whose centre contrast is the initial incumbent
+    # (solver.py:93-94: the same point)
+    ev_b = (lambda lo, hi: _split_eval(bounds, (lo, hi), group)) if split else bounds
+    root_bound = float(np.asarray(ev_b(np.array([dom.lo]), np.array([dom.hi])))[0])
+    evaluate([root])
     nu_hat, c_hat = dom.center, cache[root][0]
     ctr = itertools.count()
     heap = [(-root_bound, next(ctr), dom.lo, dom.hi)]
@@ -357,8 +386,8 @@ def solve_spec_dist(batch, params, slots_per_rank: int = 4, group=None,
     view = SimpleNamespace(n=int(t.numel()), tau=tau, geometry=geometry)
     contrasts, bounds = gpu_evaluators(view, ctx=ctx)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    return solve_spec(view, params, slots=slots_per_rank * world, contrasts=contrasts,
-                      bounds=bounds, group=group, split=world > 1)
+    return solve_spec(view, params, slots=slots_per_rank * world, bounds=bounds,
+                      nodes=gpu_node_evaluator(view, ctx=ctx), group=group, split=world > 1)
 
 
 def divergence_of(result, tau: float) -> float:

@@ -357,3 +357,25 @@ def test_root_certificate(bnb_golden, monkeypatch, cert, rng):
     r = evd.maximise_contrast_bnb(small, evd.SolverParams(min_interval_width=3.0))
     o = orc.maximise_contrast_bnb(small, min_interval_width=3.0)
     assert (r.nu, r.contrast, r.bound_gap, r.iterations) == (o.nu, o.contrast, o.bound_gap, 1)
+
+
+def test_node_terms_vs_oracle(rng):
+    """evd_eval_nodes (the solve kernel's rounds without the search): the
+    centre contrast and both children's c_bar of k nodes, bit-identical to the
+    reference's contrast_at / bound_terms, for k = 1, 3, 4, 9 (several rounds
+    of slots) on a golden-sized window and a random one; inadmissible
+    endpoints raise like the reference."""
+    from paper_2209_13168_b200.geometry import CheiralityError
+    for b in (synth.config_window(1), random_batch(rng, 40, 30, 700)):
+        dom = velocity_domain(b.tau)
+        for k in (1, 3, 4, 9):
+            lo = rng.uniform(dom.lo, dom.hi, k)
+            hi = np.minimum(lo + rng.choice([1e-6, 1e-3, 0.1, 1.0], k), dom.hi)
+            con_, ca, cb = con.node_terms(b, lo, hi)
+            for j in range(k):
+                c = 0.5 * (lo[j] + hi[j])
+                assert con_[j] == orc.contrast_at(b, c)
+                assert ca[j] == orc.bound_terms(b, lo[j], c)[2]
+                assert cb[j] == orc.bound_terms(b, c, hi[j])[2]
+    with pytest.raises(CheiralityError):
+        con.node_terms(b, [-2.5], [-0.1])
