@@ -196,6 +196,17 @@ int evd_eval_nodes(evd_ctx *ctx, const double *lo, const double *hi, int64_t k,
  * when max_iterations is reached. */
 int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *res);
 
+/* maximise_contrast_bnb (solver.py:79-123) for the window x, y, t (host,
+ * pinned or device memory; evd_set_events' arguments) in one call: upload,
+ * centring and solve are queued back to back with one host synchronisation
+ * (builds with -DEVD_PROGRESSIVE=1 launch the solve first and let its first
+ * round take each batch as its chunk arrives).  Same results as
+ * evd_set_events + evd_solve; the window stays resident.  The inputs are not
+ * retained. */
+int evd_solve_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
+                     int32_t width, int32_t height, double tau, const evd_solve_params *params,
+                     evd_solve_result *res);
+
 /* Many windows in one launch (estimate_stream_divergence, solver.py:139-162):
  * window w is events [offsets[w], offsets[w+1]) of the resident event set
  * (evd_set_events with all windows concatenated; they share width, height,

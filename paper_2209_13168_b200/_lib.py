@@ -32,7 +32,7 @@ SYMBOLS = (
     "evd_point_images", "evd_bound_images", "evd_eval_frontier", "evd_set_option",
     "evd_frontier_info", "evd_image_contrast",
     "evd_rasterize_segments",
-    "evd_eval_nodes", "evd_solve", "evd_solve_windows", "evd_solve_windows_list", "evd_solve_trace", "evd_solve_block_trace",
+    "evd_eval_nodes", "evd_solve", "evd_solve_events", "evd_solve_windows", "evd_solve_windows_list", "evd_solve_trace", "evd_solve_block_trace",
     "evd_probe_events", "evd_solve_stream", "evd_solve_loaded_stream", "evd_load_bin",
     "evd_stream_copy", "evd_load_stream", "evd_pixel_counts", "evd_stream_remove_hot_pixels",
     "evd_stream_rescale",
@@ -107,6 +107,8 @@ _SIGS = {
     "evd_rasterize_segments": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _i32, _u32p]),
     "evd_eval_nodes": (ctypes.c_int, [_vp, _d, _d, _i64, _d, _d, _d]),
     "evd_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
+    "evd_solve_events": (ctypes.c_int, [_vp, _d, _d, _d, _i64, _i32, _i32, _f64,
+                                        ctypes.POINTER(SolveParams), ctypes.POINTER(SolveResult)]),
     "evd_solve_windows": (ctypes.c_int, [_vp, _i64p, _i32, _i32, ctypes.POINTER(SolveParams),
                                          ctypes.POINTER(WindowResult), _d]),
     "evd_solve_windows_list": (ctypes.c_int, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_d),

@@ -894,7 +894,27 @@ struct EventJob {
     // segment (the root bound's certificate, k_solve_spec)
     unsigned long long *acc_root;
     double *pf;  // PF: this warp's staging buffer, [x | y | t] x 32 events
+    // progressive upload (SolveArgs::arrive), first round only: raw x, y
+    // arrive in the window buffers; the pass centres them in place
+    const unsigned long long *arrive;
 };
+
+// Progressive upload (evd_solve_events: the first round's pass takes each
+// batch as its chunk arrives, centring in place).  Off: correct (every GPU
+// test) but the extra live state in the event pass costs the resident-window
+// solve 1.3% (cfg 2 3.03 -> 3.07 ms, cfg 3 15.79 -> 15.99 ms) for an end-to-
+// end gain of 0.7-1.5% (cfg 2 3.21 -> 3.19 ms, cfg 3 16.35 -> 16.12 ms), no
+// better than queueing upload and solve back to back (tools/ab_e2e.py).
+#ifndef EVD_PROGRESSIVE
+#define EVD_PROGRESSIVE 0
+#endif
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src)
 {
@@ -966,7 +986,28 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
             }
             if (lane == 0) nb = warps * first + (long long)atomicAdd(acc + 7, (unsigned long long)nsize);
         }
+#if EVD_PROGRESSIVE
+        if (j.arrive) {  // progressive upload: wait for this batch's events
+            const long long need = base + size < n ? base + size : n;
+            if (lane == 0)
+                while ((long long)ld_acquire_u64(j.arrive) < need) __nanosleep(200);
+            __syncwarp();
+        }
+#endif
         if (lane < size && i < n) {
+#if EVD_PROGRESSIVE
+            if (!PF && j.arrive) {
+                // arriving data: raw coordinates read through L2 (no L1 line
+                // of this buffer exists yet), centred as k_center does
+                // (geometry.py:87) and written back for the later rounds; each
+                // event belongs to exactly one batch of the pass
+                x = dsub(__ldcg(xc + i), j.cx);
+                y = dsub(__ldcg(yc + i), j.cy);
+                t = __ldcg(tw + i);
+                const_cast<double *>(xc)[i] = x;
+                const_cast<double *>(yc)[i] = y;
+            } else
+#endif
             if (!PF) {
                 x = __ldg(xc + i);
                 y = __ldg(yc + i);
@@ -1883,7 +1924,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 unsigned long long v[4] = {0, 0, 0, 0}, vex[1] = {0};
                 EventJob J{xc, yc, tw, n, sl.lo, sl.c, sl.hi, sl.den_lo, sl.den_c, sl.den_hi,
                            a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
-                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1], pfbuf};
+                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1], pfbuf,
+                           it == 0 ? a.arrive : nullptr};
                 event_pass_exact<chunk_for(NT), spec_prefetch<NT>()>(J, wq, v, vex);
 #pragma unroll
                 for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 import time
 from dataclasses import dataclass
 
@@ -110,14 +111,33 @@ def solve_loaded(ctx, params: SolverParams):
     return res, ctx.launches - before
 
 
+def solve_events(ctx, batch: EventBatch, params: SolverParams):
+    """evd_solve_events: upload the window and solve it in one call, the
+    events arriving while the solve already runs; returns (SolveResult,
+    launches).  The window stays resident in ``ctx``."""
+    g = batch.geometry
+    x, y, t = _lib.f64(batch.x), _lib.f64(batch.y), _lib.f64(batch.t)
+    p = _lib.SolveParams(float(params.gamma), float(params.epsilon),
+                         float(params.min_interval_width), int(params.max_iterations))
+    if os.environ.get("EVD_LIB") and not hasattr(ctx.lib, "evd_solve_events"):
+        return solve_loaded(load_window(batch, ctx, cache=False), params)  # older build (A/B)
+    res = _lib.SolveResult()
+    ctx._resident = None
+    before = ctx.launches
+    rc = ctx.lib.evd_solve_events(ctx.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t), t.size, g.width,
+                                  g.height, float(batch.tau), p, res)
+    if rc:
+        _raise(ctx, rc, res)
+    return res, ctx.launches - before
+
+
 def solve_window(batch: EventBatch, params: SolverParams, ctx=None) -> tuple[BnbResult, SolveStats]:
     """maximise_contrast_bnb plus explored-node statistics."""
     if batch.n == 0:
         raise NoEventsError("no events in batch")
     start = time.perf_counter()
     velocity_domain(batch.tau, params.epsilon)  # ValueError on bad tau / epsilon (geometry.py:63-66)
-    ctx = load_window(batch, ctx, cache=False)
-    res, launches = solve_loaded(ctx, params)
+    res, launches = solve_events(ctx or _lib.context(), batch, params)
     runtime = time.perf_counter() - start
     return (BnbResult(res.nu, res.contrast, res.bound_gap, int(res.iterations), runtime),
             SolveStats(int(res.iterations), int(res.bound_evals), int(res.point_evals),
