@@ -1134,6 +1134,7 @@ struct Replica {
     // entries pushed by the current step (indices fr_n_before + k)
     int n_pushed;
     FrontierEntry pushed[2];
+    double root_L;  // kModeRootCert: certified lower bound of the root's c_bar
 };
 
 constexpr int kFrView = 1024;  // frontier entries staged in shared memory per step
@@ -1171,13 +1172,32 @@ __device__ void bnb_step(const SolveArgs &a, Replica &R, double S, const Frontie
         R.n_pending = 0;
         R.n_pushed = 0;
         R.point_evals++;
+        bool node = R.mode == kModeNode;
         if (R.mode == kModeRoot) {
             R.c_hat = C;
             R.nu_hat = R.c;
             const double cb = dsub(ddiv((double)R.sA, M), R.p2A);
             R.bound_evals++;
             replica_push(a, R, n0, cb, R.lo, R.hi);
-        } else {
+        } else if (R.mode == kModeRootCert) {
+            // solver.py:92-108 with the root bound certified (k_solve_spec's
+            // kModeRootCert): the root is pushed and popped at once, then
+            // evaluated as a node from this step's results
+            R.c_hat = C;
+            R.nu_hat = R.c;
+            R.point_evals++;
+            R.bound_evals++;
+            R.next_counter++;
+            if (n0 + 1 > R.max_fr) R.max_fr = n0 + 1;
+            if (!(R.root_L - C > a.gamma + 1e-9 * fabs(C))) {
+                R.status = kStatusRootCert;
+                R.done = 1;
+            } else {
+                R.iterations++;
+                node = true;
+            }
+        }
+        if (node) {
             if (C >= R.c_hat) {  // solver.py:111
                 R.nu_hat = R.c;
                 R.c_hat = C;
@@ -1443,9 +1463,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
         if (gb == 0 && threadIdx.x == 0) {
             unsigned long long *z = &st->acc[0][0];
             for (int k = 0; k < 16; k++) __stcg(z + k, 0ull);
+            __stcg(&st->sacc[0][1][0], 0ull);  // kModeRootCert sums
+            __stcg(&st->sacc[0][1][1], 0ull);
         }
         grid_sync(ctr, target, GB);
         if (threadIdx.x == 0) {
+            R.root_L = 0.0;
             R.lo = a.lo0;
             R.hi = a.hi0;
             R.c = a.c0;
@@ -1455,7 +1478,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
             R.r_lo = ddiv(1.0, R.den_lo);
             R.r_c = ddiv(1.0, R.den_c);
             R.r_hi = ddiv(1.0, R.den_hi);
-            R.mode = kModeRoot;
+            R.mode = a.root_cert ? kModeRootCert : kModeRoot;
             R.done = 0;
             R.status = kStatusOk;
             R.parity = 0;
@@ -1493,7 +1516,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
             // both give the same images
             if (!FILTER || dsub(hi, lo) > kFilterWidth) {
                 EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
-                           W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth};
+                           W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth,
+                           &st->sacc[0][1][0]};
                 event_pass_exact<chunk_for(NT)>(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
@@ -1671,6 +1695,12 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
                 const unsigned long long in_image = __ldcg(acc);
                 R.sA = a45.x;
                 R.sB = a45.y;
+                if (mode == kModeRootCert) {  // as k_solve_spec: S >= sum^2 / M
+                    const double Md = (double)tree.M;
+                    const double q = (double)__ldcg(&st->sacc[0][1][0]) / Md;
+                    const double f = (double)__ldcg(&st->sacc[0][1][1]) / Md;
+                    R.root_L = (q * q - f * f) * (1.0 - 1e-9);  // compared in bnb_step
+                }
                 R.marks += in_image + a23.y;
                 R.exact += a67.x;
                 if (tr && gb == 0 && it < a.trace_iters) {  // per-node work counters

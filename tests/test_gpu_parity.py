@@ -322,17 +322,19 @@ def test_bound_validity_properties_full_size(cfg):
         assert fi[2] == ins[0]
 
 
+@pytest.mark.parametrize("k", ["1", "4"])
 @pytest.mark.parametrize("cert", ["on", "off"])
-def test_root_certificate(bnb_golden, monkeypatch, cert, rng):
+def test_root_certificate(bnb_golden, monkeypatch, cert, k, rng):
     """The speculative solve certifies the root bound (S >= (sum of per-event
     cell lower bounds)^2 / M) instead of rasterising it; a window whose
     certificate fails (few events: the bound is not provably above c_hat +
     gamma) is rerun with the root rasterised.  Results equal the reference's
-    either way, including iteration limits at the root and a root narrower
-    than min_interval_width (whose exact bound is the reported bound_gap)."""
+    either way, in both solve kernels, including iteration limits at the root
+    and a root narrower than min_interval_width (whose exact bound is the
+    reported bound_gap); grouped many-window solves too."""
     if cert == "off":
         monkeypatch.setenv("EVD_NO_ROOT_CERT", "1")
-    monkeypatch.setenv("EVD_SPEC_K", "4")
+    monkeypatch.setenv("EVD_SPEC_K", k)  # 1: k_solve, 4: k_solve_spec
     meta, windows = bnb_golden
     for w, batch in windows:
         assert _same(evd.maximise_contrast_bnb(batch, evd.SolverParams()), w["result"])
@@ -353,6 +355,15 @@ def test_root_certificate(bnb_golden, monkeypatch, cert, rng):
         evd.maximise_contrast_bnb(b, evd.SolverParams(max_iterations=1))
     o = orc.maximise_contrast_bnb(b, max_iterations=1)
     assert (err.value.nu, err.value.contrast, err.value.iterations) == (o.nu, o.contrast, 1)
+    seq = gold["sequence"]
+    wins = [synth.sequence_window(q["k"]) for q in seq]
+    w0 = wins[0]
+    tiny = EventBatch(w0.x[:2], w0.y[:2], w0.t[:2], w0.tau, w0.geometry)  # certificate fails
+    res, _, _ = sol.solve_windows(wins + [tiny], evd.SolverParams(), groups=3)
+    for r, q in zip(res, seq):
+        assert r.status == 0 and _same(r, q["result"])
+    o = orc.maximise_contrast_bnb(tiny)
+    assert (res[-1].nu, res[-1].contrast, res[-1].iterations) == (o.nu, o.contrast, o.iterations)
     small = windows[0][1]
     r = evd.maximise_contrast_bnb(small, evd.SolverParams(min_interval_width=3.0))
     o = orc.maximise_contrast_bnb(small, min_interval_width=3.0)
