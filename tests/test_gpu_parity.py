@@ -390,3 +390,38 @@ def test_node_terms_vs_oracle(rng):
                 assert cb[j] == orc.bound_terms(b, c, hi[j])[2]
     with pytest.raises(CheiralityError):
         con.node_terms(b, [-2.5], [-0.1])
+
+
+def test_solve_events_sources(bnb_golden):
+    """evd_solve_events (maximise_contrast_bnb's one-call path) from pageable
+    host, pinned host and device arrays gives the reference's result, leaves
+    the window resident for the per-call entry points, and reports an empty
+    window like the reference."""
+    import ctypes
+    import torch
+    with open(os.path.join(GOLDEN, "bnb.json")) as fh:
+        ref = json.load(fh)["configs"]["1"]["result"]
+    b = synth.config_window(1)
+    g = b.geometry
+    ctx = _lib.context()
+    p = evd.SolverParams()
+    r, _ = sol.solve_events(ctx, b, p)  # pageable numpy arrays
+    assert _same(r, ref)
+    sp = _lib.SolveParams(p.gamma, p.epsilon, p.min_interval_width, p.max_iterations)
+    ptr = lambda v: ctypes.cast(v.data_ptr(), ctypes.POINTER(ctypes.c_double))
+    for kind in ("pinned", "device"):
+        ts = {k: torch.from_numpy(np.ascontiguousarray(getattr(b, k))) for k in "xyt"}
+        ts = {k: (v.pin_memory() if kind == "pinned" else v.cuda()) for k, v in ts.items()}
+        torch.cuda.synchronize()
+        res = _lib.SolveResult()
+        rc = ctx.lib.evd_solve_events(ctx.h, ptr(ts["x"]), ptr(ts["y"]), ptr(ts["t"]), b.n,
+                                      g.width, g.height, b.tau, sp, res)
+        assert rc == 0 and _same(res, ref), kind
+    # the window stays resident: a per-call bound on it needs no upload
+    dom = velocity_domain(b.tau)
+    sb, fi, _ = con.frontier_terms(b, [dom.lo], [dom.center], ctx=ctx, loaded=True)
+    o = orc.bound_terms(b, dom.lo, dom.center)
+    assert float(sb[0]) == o[0] and int(fi[0]) == o[3]
+    empty = EventBatch(np.empty(0), np.empty(0), np.empty(0), 0.5, SensorGeometry(8, 8))
+    with pytest.raises(evd.NoEventsError):
+        evd.maximise_contrast_bnb(empty, p)
