@@ -1343,9 +1343,10 @@ int evd_solve_events(evd_ctx *ctx, const double *x, const double *y, const doubl
     int rc = run_windows(ctx, off, 1, 1, params, out, &ms, nullptr, nullptr, &prog);
     // inputs are never retained: the copies are done before returning
     cudaError_t ce = cudaStreamSynchronize(ctx->copy);
-    if (ce != cudaSuccess || (rc && rc != EVD_ERR_ITER_LIMIT && rc != EVD_ERR_CHEIRALITY &&
-                              rc != EVD_ERR_ARG)) {
-        ctx->n = -1;  // the window may be incomplete: nothing is resident
+    if (ce != cudaSuccess || (rc && rc != EVD_ERR_ITER_LIMIT)) {
+        // a parameter error returns before the upload, a CUDA error may stop
+        // it half-way: either way nothing is resident
+        ctx->n = -1;
         ctx->gen++;
     }
     if (rc) return rc;
