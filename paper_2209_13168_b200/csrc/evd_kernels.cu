@@ -38,7 +38,23 @@ constexpr int kChunk = EVD_CHUNK;
 #ifndef EVD_CHUNK_LARGE
 #define EVD_CHUNK_LARGE 24
 #endif
+#ifndef EVD_DRAIN_CONT
+#define EVD_DRAIN_CONT 1
+#endif
+#ifndef EVD_DRAIN_RELOAD
+#define EVD_DRAIN_RELOAD 1
+#endif
+#ifndef EVD_DRAIN_CONT_MAXNT
+#define EVD_DRAIN_CONT_MAXNT 1024
+#endif
 constexpr int chunk_for(int nt) { return nt >= 768 ? EVD_CHUNK_LARGE : kChunk; }
+// warp_drain's continuing cursors (EVD_DRAIN_CONT; the segment re-read from
+// shared memory each round, EVD_DRAIN_RELOAD): cfg 1 0.758 -> 0.748 ms, cfg 2
+// 3.038 -> 2.985 ms, cfg 3 15.80 -> 15.77 ms, cfg 5 128.8 -> 125.6 ms; the
+// cfg-2 root-width event pass 147 -> 128 us (tools/probe_events.py).  Kept
+// per CTA size (EVD_DRAIN_CONT_MAXNT) for A/B.
+template <int NT>
+constexpr bool drain_cont() { return EVD_DRAIN_CONT && NT <= EVD_DRAIN_CONT_MAXNT; }
 #ifndef EVD_PIX_CUT_THREADS
 #define EVD_PIX_CUT_THREADS 128
 #endif
@@ -144,6 +160,7 @@ __device__ __forceinline__ int segment_or_queue(double ax, double ay, double bx,
 // Sample every chunk the warp queued, in rounds of 32: all lanes position
 // their cursors together, then step one item per iteration; chunks hold
 // nearly equal item counts, so the lanes stay converged.
+template <bool CONT = EVD_DRAIN_CONT>
 __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int H)
 {
     const int lane = threadIdx.x & 31;
@@ -159,6 +176,51 @@ __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int 
     __syncwarp();
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int marks = 0;
+    if (CONT) {
+    // Lane l takes chunks l*R .. l*R + R-1, one per round: consecutive chunks
+    // of a segment stay on one lane, whose cursor simply runs on (the state a
+    // chunk's last step leaves is the state cursor_init would compute for the
+    // next: same items, same lookahead, prev = the last midpoint's range), so
+    // only a lane's first chunk of each segment pays the merge-path search.
+    const int R = (total + 31) >> 5;
+    int pslot = -1, pj = -1;
+    Cursor c;
+    SegDesc d;
+    AtomicSink sink{nullptr};
+    for (int r = 0; r < R; r++) {
+        const int t = lane * R + r;
+        bool active = false;
+        if (t < total) {
+            int L = 0;  // largest lane with off[L] <= t
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1)
+                if (q.off[L + s] <= t) L += s;
+            const int rr = t - q.off[L];
+            const bool second = rr >= q.na[L];
+            const int slot = 2 * L + (second ? 1 : 0), j = second ? rr - q.na[L] : rr;
+            if (slot == pslot && j == pj + 1) {
+#if EVD_DRAIN_RELOAD
+                d = q.d[slot];  // not live across rounds
+#endif
+                const int N = d.X.n + d.Y.n + 2, m0 = j * d.csize;
+                c.left = N - m0 < d.csize ? N - m0 : d.csize;
+                c.fin = c.kind == 0 ? 1 : 0;  // the chunk holds only the trailing sample
+                active = true;
+            } else {
+                d = q.d[slot];
+                sink.img = q.img[slot];
+                active = cursor_init(d, j, c);
+            }
+            pslot = slot;
+            pj = j;
+        }
+        const bool live = active;
+        if (active) active = cursor_head(d, c, W, H, sink, marks);
+        while (__any_sync(0xffffffffu, active))
+            if (active) active = cursor_step(d, c, W, H, sink, marks);
+        if (live) cursor_tail(d, c, W, H, sink, marks);
+    }
+    } else {
     for (int base = 0; base < total; base += 32) {
         const int t = base + lane;
         bool active = false;
@@ -182,6 +244,7 @@ __device__ __noinline__ int warp_drain(WarpQueue &q, int cA, int cB, int W, int 
         while (__any_sync(0xffffffffu, active))
             if (active) active = cursor_step(d, c, W, H, sink, marks);
         if (live) cursor_tail(d, c, W, H, sink, marks);
+    }
     }
     __syncwarp();
     return marks;
@@ -925,7 +988,7 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src)
 // PF: the next batch's events are claimed when a batch starts and staged into
 // shared memory (cp.async) while the batch's segments are built and sampled,
 // so neither the claim's nor the loads' L2 round trip is on the warp's path.
-template <int C = kChunk, bool PF = false>
+template <int C = kChunk, bool PF = false, bool CONT = EVD_DRAIN_CONT>
 __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &wq,
                                                  unsigned long long (&v)[4],
                                                  unsigned long long (&vex)[1])
@@ -1040,7 +1103,7 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
             nb = __shfl_sync(0xffffffffu, nb, 0);
             if (nb < n) stage(nb, nsize);
         }
-        if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain(wq, cA, cB, W, H);
+        if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain<CONT>(wq, cA, cB, W, H);
         v[3] += dummy;
         if (PF) {
             base = nb;
@@ -1518,7 +1581,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
                 EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
                            W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth,
                            &st->sacc[0][1][0]};
-                event_pass_exact<chunk_for(NT)>(J, wq, v, vex);
+                event_pass_exact<chunk_for(NT), false, drain_cont<NT>()>(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
                 long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
@@ -1595,7 +1658,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
                             }
                         }
                         if (__any_sync(0xffffffffu, (cA | cB) != 0))
-                            dummy += warp_drain(wq, cA, cB, W, H);
+                            dummy += warp_drain<drain_cont<NT>()>(wq, cA, cB, W, H);
                     }
                     v[3] += dummy;
                     if (!more && nq == 0) break;
@@ -1956,7 +2019,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                            a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
                            gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1], pfbuf,
                            it == 0 ? a.arrive : nullptr};
-                event_pass_exact<chunk_for(NT), spec_prefetch<NT>()>(J, wq, v, vex);
+                event_pass_exact<chunk_for(NT), spec_prefetch<NT>(), drain_cont<NT>()>(J, wq, v,
+                                                                                     vex);
 #pragma unroll
                 for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);
                 vex[0] = warp_sum(vex[0]);
