@@ -31,12 +31,14 @@ constexpr int kSolveThreads = EVD_SOLVE_THREADS;
 #define EVD_CHUNK 16
 #endif
 constexpr int kChunk = EVD_CHUNK;
-// The solve's 768-thread build (windows from 250 k events) samples in chunks
-// of 24: cfg 3 18.10 -> 17.96 ms, cfg 5 147.5 -> 144.3 ms; 16 stays best
-// below (cfg 1 0.947 vs 0.971 ms at 24, cfg 2 neutral).  Chunk size only
-// moves the seams, never the marks.
+// Chunk size of the 768-thread build (windows from 250 k events): 24 was best
+// while every chunk paid a merge-path search (cfg 3 18.10 -> 17.96 ms vs 16);
+// with continuing cursors (warp_drain) 16 is: cfg 3 15.79 -> 15.58 ms, cfg 5
+// 125.4 -> 124.2 ms (12: 15.65 / 125.1, 8: 16.09 / 129.6, 32: 16.04 ms).  At
+// 384 / 512 threads 16 stays (12: cfg 1 0.748 -> 0.755 ms, cfg 2 2.99 ->
+// 2.98 ms).  Chunk size only moves the seams, never the marks.
 #ifndef EVD_CHUNK_LARGE
-#define EVD_CHUNK_LARGE 24
+#define EVD_CHUNK_LARGE 16
 #endif
 #ifndef EVD_DRAIN_CONT
 #define EVD_DRAIN_CONT 1
