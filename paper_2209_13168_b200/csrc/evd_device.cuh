@@ -253,6 +253,17 @@ __device__ __forceinline__ int mark_point(double px, double py, int W, int H, Pr
     return marks;
 }
 
+// the segment end samples' calls (cursor_head / cursor_tail): the general
+// closed-square call, or mark_interior (same marks: its single-cell fast path
+// is mark_point's result for a point off the grid lines)
+#ifndef EVD_END_INTERIOR
+#define EVD_END_INTERIOR 1
+#endif
+#if EVD_END_INTERIOR
+#define EVD_END_MARK mark_interior
+#else
+#define EVD_END_MARK mark_point
+#endif
 // mark_point for a point that is usually inside one pixel (a midpoint
 // between consecutive crossings): the single-cell case tests one pixel;
 // points on a grid line take the general path.
@@ -622,7 +633,7 @@ __device__ __forceinline__ bool cursor_head(const SegDesc &d, Cursor &c, int W, 
 {
     if (c.fin) return false;
     if (c.kind == 0)
-        marks += mark_point(dadd(d.X.c0, dmul(0.0, d.X.dd)), dadd(d.Y.c0, dmul(0.0, d.Y.dd)), W,
+        marks += EVD_END_MARK(dadd(d.X.c0, dmul(0.0, d.X.dd)), dadd(d.Y.c0, dmul(0.0, d.Y.dd)), W,
                             H, c.prev, sink);  // p(0), the reference's expression
     return true;
 }
@@ -634,7 +645,7 @@ __device__ __forceinline__ void cursor_tail(const SegDesc &d, const Cursor &c, i
 {
     if (c.fin) {
         Prev prev = c.prev;
-        marks += mark_point(dadd(d.X.c0, dmul(1.0, d.X.dd)), dadd(d.Y.c0, dmul(1.0, d.Y.dd)), W, H,
+        marks += EVD_END_MARK(dadd(d.X.c0, dmul(1.0, d.X.dd)), dadd(d.Y.c0, dmul(1.0, d.Y.dd)), W, H,
                             prev, sink);
     }
 }
