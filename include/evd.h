@@ -198,11 +198,9 @@ int evd_solve(evd_ctx *ctx, const evd_solve_params *params, evd_solve_result *re
 
 /* maximise_contrast_bnb (solver.py:79-123) for the window x, y, t (host,
  * pinned or device memory; evd_set_events' arguments) in one call: upload,
- * centring and solve are queued back to back with one host synchronisation
- * (builds with -DEVD_PROGRESSIVE=1 launch the solve first and let its first
- * round take each batch as its chunk arrives).  Same results as
- * evd_set_events + evd_solve; the window stays resident.  The inputs are not
- * retained. */
+ * centring and solve are queued back to back with one host synchronisation.
+ * Same results as evd_set_events + evd_solve; the window stays resident.  The
+ * inputs are not retained. */
 int evd_solve_events(evd_ctx *ctx, const double *x, const double *y, const double *t, int64_t n,
                      int32_t width, int32_t height, double tau, const evd_solve_params *params,
                      evd_solve_result *res);

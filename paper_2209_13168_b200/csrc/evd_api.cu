@@ -133,7 +133,6 @@ struct evd_ctx {
     cudaEvent_t feed_start = nullptr;
     DevBuf<unsigned long long> feedw;         // [0] raw events delivered, [1] stall flag
     DevBuf<long long> feedb;                  // per window: raw lo, count, unpadded offsets
-    unsigned long long *arrive_host = nullptr; // evd_solve_events: pinned per-chunk counts
 };
 
 namespace {
@@ -507,7 +506,6 @@ void evd_destroy(evd_ctx *ctx)
     if (ctx->feed_start) cudaEventDestroy(ctx->feed_start);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->stage) cudaFreeHost(ctx->stage);
-    if (ctx->arrive_host) cudaFreeHost(ctx->arrive_host);
     for (cudaEvent_t e : ctx->stage_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1033,14 +1031,10 @@ struct EvalList {
     double *out;
 };
 
-// evd_solve_events: the window's upload, queued before the solve (default
-// build) or while it runs (EVD_PROGRESSIVE builds, SolveArgs::arrive)
-#ifndef EVD_PROGRESSIVE
-#define EVD_PROGRESSIVE 0
-#endif
+// evd_solve_events: the window's upload, queued on the copy stream before
+// the solve (run_windows calls it right before the launch)
 struct Progressive {
-    const unsigned long long *arrive;
-    std::function<int()> upload;  // queues the chunks on ctx->copy
+    std::function<int()> upload;  // queues the window's copies on ctx->copy
 };
 
 static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int groups,
@@ -1179,20 +1173,16 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
         }
         const bool spec_launch = spec_k > 1 || ev || getenv("EVD_SPEC_FORCE");
         if (prog && prog->upload) {
-            if (spec_launch && EVD_PROGRESSIVE) {
-                a.arrive = prog->arrive;  // the first round's pass waits per batch
-            } else {
-                // the solve reads centred events from its first node on:
-                // upload, then centre on the solve's stream
-                const int urc = prog->upload();
-                prog->upload = nullptr;
-                if (urc) return urc;
-                CU(cudaEventRecord(ctx->feed_start, ctx->copy));
-                CU(cudaStreamWaitEvent(ctx->stream, ctx->feed_start, 0));
-                launch_center(ctx->xc.p, ctx->yc.p, ctx->n, ctx->W / 2.0, ctx->H / 2.0, ctx->xc.p,
-                              ctx->yc.p, ctx->stream);
-                LAUNCHED(1);
-            }
+            // the solve reads centred events from its first node on: upload,
+            // then centre on the solve's stream
+            const int urc = prog->upload();
+            prog->upload = nullptr;
+            if (urc) return urc;
+            CU(cudaEventRecord(ctx->feed_start, ctx->copy));
+            CU(cudaStreamWaitEvent(ctx->stream, ctx->feed_start, 0));
+            launch_center(ctx->xc.p, ctx->yc.p, ctx->n, ctx->W / 2.0, ctx->H / 2.0, ctx->xc.p,
+                          ctx->yc.p, ctx->stream);
+            LAUNCHED(1);
         }
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
         CU(spec_launch
@@ -1200,19 +1190,6 @@ static int run_windows(evd_ctx *ctx, const long long *off, int n_windows, int gr
                : launch_solve(a, groups * GB, threads, ctx->stream));
         LAUNCHED(1);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
-        if (prog && prog->upload) {
-            const int urc = prog->upload();
-            prog->upload = nullptr;
-            if (urc) {
-                // release the waiting solve (its window is garbage), then report
-                static const unsigned long long all = ~0ull;
-                cudaMemcpy(const_cast<unsigned long long *>(prog->arrive), &all, sizeof all,
-                           cudaMemcpyHostToDevice);
-                cudaStreamSynchronize(ctx->copy);
-                cudaStreamSynchronize(ctx->stream);
-                return urc;
-            }
-        }
         if (feed && feed->upload) {
             // the solve waits on the chunks: feed them now (host copies into
             // pinned slots, device copies on ctx->copy)
@@ -1290,7 +1267,6 @@ int evd_solve_events(evd_ctx *ctx, const double *x, const double *y, const doubl
     CU(ctx->xc.ensure(n));
     CU(ctx->yc.ensure(n));
     CU(ctx->t.ensure(n));
-    CU(ctx->feedw.ensure(2));
     if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
     if (!ctx->feed_start) {
         CU(cudaEventCreateWithFlags(&ctx->feed_start, cudaEventDisableTiming));
@@ -1301,40 +1277,16 @@ int evd_solve_events(evd_ctx *ctx, const double *x, const double *y, const doubl
     ctx->W = width;
     ctx->H = height;
     ctx->tau = tau;
-    // the chunks start after everything queued so far (earlier readers of
-    // the window buffers) and after the arrival counter is reset
-    CU(cudaMemsetAsync(ctx->feedw.p, 0, sizeof(unsigned long long), ctx->stream));
+    // the copies start after everything queued so far (earlier readers of
+    // the window buffers); run_windows queues them on the copy stream right
+    // before the launch, the centring and the solve after them on ctx->stream
     CU(cudaEventRecord(ctx->feed_start, ctx->stream));
     CU(cudaStreamWaitEvent(ctx->copy, ctx->feed_start, 0));
-    // chunks of feed_chunk events (at most kArriveSlots); after each chunk's
-    // raw x, y, t the count of events delivered goes up by DMA from a pinned
-    // slot (copy engines only: the persistent solve holds every SM)
-    constexpr int kArriveSlots = 64;
-    if (!ctx->arrive_host)
-        CU(cudaHostAlloc(&ctx->arrive_host, kArriveSlots * sizeof(unsigned long long),
-                         cudaHostAllocDefault));
-#if EVD_PROGRESSIVE
-    const long long S = std::max<long long>(
-        {16LL, (long long)ctx->feed_chunk, (long long)((n + kArriveSlots - 1) / kArriveSlots)});
-#else
-    // default build: the window goes up as one chunk before the solve starts
-    // (queued back to back with it on the copy stream, one host sync for both)
-    const long long S = n;
-#endif
-    Progressive prog{ctx->feedw.p, nullptr};
+    Progressive prog;
     prog.upload = [&]() -> int {
-        for (long long c0 = 0, c = 0; c0 < n; c0 += S, c++) {
-            const long long m = std::min(S, n - c0);
-            CU(cudaMemcpyAsync(ctx->xc.p + c0, x + c0, m * sizeof(double), cudaMemcpyDefault,
-                               ctx->copy));
-            CU(cudaMemcpyAsync(ctx->yc.p + c0, y + c0, m * sizeof(double), cudaMemcpyDefault,
-                               ctx->copy));
-            CU(cudaMemcpyAsync(ctx->t.p + c0, t + c0, m * sizeof(double), cudaMemcpyDefault,
-                               ctx->copy));
-            ctx->arrive_host[c] = (unsigned long long)(c0 + m);
-            CU(cudaMemcpyAsync(ctx->feedw.p, ctx->arrive_host + c, sizeof(unsigned long long),
-                               cudaMemcpyHostToDevice, ctx->copy));
-        }
+        CU(cudaMemcpyAsync(ctx->xc.p, x, n * sizeof(double), cudaMemcpyDefault, ctx->copy));
+        CU(cudaMemcpyAsync(ctx->yc.p, y, n * sizeof(double), cudaMemcpyDefault, ctx->copy));
+        CU(cudaMemcpyAsync(ctx->t.p, t, n * sizeof(double), cudaMemcpyDefault, ctx->copy));
         return EVD_OK;
     };
     const long long off[2] = {0, n};

@@ -101,11 +101,6 @@ struct SolveArgs {
     const double *ev_lo, *ev_hi;
     long long ev_n;
     double *ev_out;
-    // progressive upload (evd_solve_events, k_solve_spec, one window): raw
-    // events [0, *arrive) are on the device; the first round's event pass
-    // waits per batch for its events, reads them through L2 (.cg) and centres
-    // x, y in place (no kernel can run beside the persistent solve)
-    const unsigned long long *arrive;
     // Overlapped stream upload (evd_solve_stream from host arrays; sx null:
     // the windows are already gathered).  The raw stream arrives in chunks on
     // a copy stream while the solve runs; *ready = raw events on the device.

@@ -958,39 +958,9 @@ struct EventJob {
     // kModeRootCert: [0] += root_cells_lb, [1] += fully_inside of the root
     // segment (the root bound's certificate, k_solve_spec)
     unsigned long long *acc_root;
-    double *pf;  // PF: this warp's staging buffer, [x | y | t] x 32 events
-    // progressive upload (SolveArgs::arrive), first round only: raw x, y
-    // arrive in the window buffers; the pass centres them in place
-    const unsigned long long *arrive;
 };
 
-// Progressive upload (evd_solve_events: the first round's pass takes each
-// batch as its chunk arrives, centring in place).  Off: correct (every GPU
-// test) but the extra live state in the event pass costs the resident-window
-// solve 1.3% (cfg 2 3.03 -> 3.07 ms, cfg 3 15.79 -> 15.99 ms) for an end-to-
-// end gain of 0.7-1.5% (cfg 2 3.21 -> 3.19 ms, cfg 3 16.35 -> 16.12 ms), no
-// better than queueing upload and solve back to back (tools/ab_e2e.py).
-#ifndef EVD_PROGRESSIVE
-#define EVD_PROGRESSIVE 0
-#endif
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void cp_async8(double *dst, const double *src)
-{
-    const unsigned int d = (unsigned int)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-
-// PF: the next batch's events are claimed when a batch starts and staged into
-// shared memory (cp.async) while the batch's segments are built and sampled,
-// so neither the claim's nor the loads' L2 round trip is on the warp's path.
-template <int C = kChunk, bool PF = false, bool CONT = EVD_DRAIN_CONT>
+template <int C = kChunk, bool CONT = EVD_DRAIN_CONT>
 __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &wq,
                                                  unsigned long long (&v)[4],
                                                  unsigned long long (&vex)[1])
@@ -1018,66 +988,15 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
     const int first = (int)(fb < 4 ? 4 : (fb > 32 ? 32 : fb));
     long long base = (j.gb * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * first;
     int size = first;
-    double *pf = j.pf;
-    auto stage = [&](long long b, int sz) {
-        const long long ii = b + lane;
-        if (lane < sz && ii < n) {
-            cp_async8(pf + lane, xc + ii);
-            cp_async8(pf + 32 + lane, yc + ii);
-            cp_async8(pf + 64 + lane, tw + ii);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    if (PF) stage(base, size);
+    // (tried and measured slower, kept out: the next batch claimed and staged
+    // into shared memory with cp.async while a batch is worked on, and the
+    // first pass consuming batches as their upload chunks arrive -- DESIGN.md
+    // §7, commits ce05e17 and 0d7c49a)
     while (base < n) {
         const long long i = base + lane;
         int cA = 0, cB = 0, dummy = 0;
-        double x = 0.0, y = 0.0, t = 0.0;
-        long long nb = 0;
-        int nsize = size;
-        if (PF) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-            if (lane < size && i < n) {
-                x = pf[lane];
-                y = pf[32 + lane];
-                t = pf[64 + lane];
-            }
-            __syncwarp();
-            if (j.guided) {
-                const long long rem = n - base;
-                long long s = rem / (2 * warps);
-                nsize = (int)(s < 4 ? 4 : (s > first ? first : s));
-            }
-            if (lane == 0) nb = warps * first + (long long)atomicAdd(acc + 7, (unsigned long long)nsize);
-        }
-#if EVD_PROGRESSIVE
-        if (j.arrive) {  // progressive upload: wait for this batch's events
-            const long long need = base + size < n ? base + size : n;
-            if (lane == 0)
-                while ((long long)ld_acquire_u64(j.arrive) < need) __nanosleep(200);
-            __syncwarp();
-        }
-#endif
         if (lane < size && i < n) {
-#if EVD_PROGRESSIVE
-            if (!PF && j.arrive) {
-                // arriving data: raw coordinates read through L2 (no L1 line
-                // of this buffer exists yet), centred as k_center does
-                // (geometry.py:87) and written back for the later rounds; each
-                // event belongs to exactly one batch of the pass
-                x = dsub(__ldcg(xc + i), j.cx);
-                y = dsub(__ldcg(yc + i), j.cy);
-                t = __ldcg(tw + i);
-                const_cast<double *>(xc)[i] = x;
-                const_cast<double *>(yc)[i] = y;
-            } else
-#endif
-            if (!PF) {
-                x = __ldg(xc + i);
-                y = __ldg(yc + i);
-                t = __ldg(tw + i);
-            }
+            const double x = __ldg(xc + i), y = __ldg(yc + i), t = __ldg(tw + i);
             const Warped wl = warp_event(x, y, t, j.lo, j.den_lo, j.cx, j.cy);
             const Warped wc = warp_event(x, y, t, j.c, j.den_c, j.cx, j.cy);
             const Warped wh = warp_event(x, y, t, j.hi, j.den_hi, j.cx, j.cy);
@@ -1101,23 +1020,15 @@ __device__ __forceinline__ void event_pass_exact(const EventJob &j, WarpQueue &w
             }
             vex[0]++;
         }
-        if (PF) {
-            nb = __shfl_sync(0xffffffffu, nb, 0);
-            if (nb < n) stage(nb, nsize);
-        }
         if (__any_sync(0xffffffffu, (cA | cB) != 0)) dummy += warp_drain<CONT>(wq, cA, cB, W, H);
         v[3] += dummy;
-        if (PF) {
-            base = nb;
-            size = nsize;
-            continue;
-        }
         if (j.guided) {
             // claim size from the remaining events as last seen by this warp
             const long long rem = n - base;
             long long s = rem / (2 * warps);
             size = (int)(s < 4 ? 4 : (s > first ? first : s));
         }
+        long long nb = 0;
         if (lane == 0) nb = warps * first + (long long)atomicAdd(acc + 7, (unsigned long long)size);
         base = __shfl_sync(0xffffffffu, nb, 0);
     }
@@ -1583,7 +1494,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
                 EventJob J{xc, yc, tw, n, lo, c, hi, den_lo, den_c, den_hi, a.cx, a.cy,
                            W, H, P, A, B, mode, acc, gsz, gb, dsub(hi, lo) > kGuidedWidth,
                            &st->sacc[0][1][0]};
-                event_pass_exact<chunk_for(NT), false, drain_cont<NT>()>(J, wq, v, vex);
+                event_pass_exact<chunk_for(NT), drain_cont<NT>()>(J, wq, v, vex);
             } else {
                 int nq = 0;  // uncertain events queued in wq.ev (warp-uniform)
                 long long base = gb * (long long)blockDim.x + (threadIdx.x & ~31);
@@ -1811,17 +1722,6 @@ __global__ void __launch_bounds__(NT, 1) k_solve(SolveArgs a_param)
 // the frontier's current best, rarely the newest children), so the per-round
 // fixed costs (two grid barriers, the contrast reduction, the step) are paid
 // ~3.5x less often.  The frontier is replicated in every CTA's shared memory.
-// Event staging (event_pass_exact PF: claim the next batch when a batch
-// starts, cp.async its x / y / t into shared memory while the batch is
-// built and sampled), off: measured slower, cfg 1 0.740 -> 0.801 ms, cfg 2
-// 3.095 -> 3.270 ms (same box, tools/ab3.sh; build with -DEVD_PREFETCH=1) --
-// the window is L2-resident, and a batch reserved one ahead idles while
-// other warps run dry at the end of each pass.
-#ifndef EVD_PREFETCH
-#define EVD_PREFETCH 0
-#endif
-template <int NT>
-constexpr bool spec_prefetch() { return EVD_PREFETCH && NT <= 512; }
 constexpr int kSpecFr = 1024;     // frontier entries per CTA (shared memory)
 constexpr int kSpecCache = 64;    // results of evaluated, not yet popped nodes
 #ifndef EVD_SPEC_WIDTH
@@ -1937,9 +1837,6 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
     double *scratch = reinterpret_cast<double *>(smem);
     TreeCache &tc = *reinterpret_cast<TreeCache *>(smem + kRegionA);
     FrontierEntry *frs = reinterpret_cast<FrontierEntry *>(smem + kRegionA + sizeof(TreeCache));
-    double *pfbuf = reinterpret_cast<double *>(smem + kRegionA + sizeof(TreeCache) +
-                                               kSpecFr * sizeof(FrontierEntry)) +
-                    (threadIdx.x >> 5) * 96;
     __shared__ SpecState Z;
     __shared__ unsigned long long s_acc[kSpecK][5];
     __shared__ int s_flag;
@@ -2019,10 +1916,8 @@ __global__ void __launch_bounds__(NT, 1) k_solve_spec(SolveArgs a)
                 unsigned long long v[4] = {0, 0, 0, 0}, vex[1] = {0};
                 EventJob J{xc, yc, tw, n, sl.lo, sl.c, sl.hi, sl.den_lo, sl.den_c, sl.den_hi,
                            a.cx, a.cy, W, H, P, A, B, (s == 0 ? mode : kModeNode), sacc[s],
-                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1], pfbuf,
-                           it == 0 ? a.arrive : nullptr};
-                event_pass_exact<chunk_for(NT), spec_prefetch<NT>(), drain_cont<NT>()>(J, wq, v,
-                                                                                     vex);
+                           gsz, gb, dsub(sl.hi, sl.lo) > kGuidedWidth, sacc[1]};
+                event_pass_exact<chunk_for(NT), drain_cont<NT>()>(J, wq, v, vex);
 #pragma unroll
                 for (int k = 0; k < 4; k++) v[k] = warp_sum(v[k]);
                 vex[0] = warp_sum(vex[0]);
@@ -2382,8 +2277,7 @@ constexpr size_t solve_smem() { return SolveSmem<NT>::region_a + sizeof(TreeCach
 template <int NT>
 constexpr size_t spec_smem()
 {
-    return SolveSmem<NT>::region_a + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry) +
-           (spec_prefetch<NT>() ? (NT / 32) * 96 * sizeof(double) : 0);
+    return SolveSmem<NT>::region_a + sizeof(TreeCache) + kSpecFr * sizeof(FrontierEntry);
 }
 
 // Kernel attributes are per device: set them once for each device a context
